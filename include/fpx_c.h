@@ -1,0 +1,153 @@
+/*
+ * fpx_c.h -- C-ABI of libfpx_b200.so, the B200-native (sm_100a) TC-FPx
+ * W6A16 linear layer.  Plain pointers and sizes only; no C++ or torch types.
+ *
+ * This is the drop-in boundary for the reference's C++ API
+ * (/root/reference/proj/include/fpx/):
+ *   fpx_quantize      <- quantize_matrix        codec.hpp:66   (codec.cpp:105-177)
+ *   fpx_prepack       <- pack                   prepack.hpp:84-85 (prepack.cpp:153-209)
+ *   fpx_unpack        <- unpack                 prepack.hpp:86  (prepack.cpp:211-260)
+ *   fpx_dequantize    <- dequantize_reference   codec.hpp:72   (codec.cpp:179-193)
+ *   fpx_linear        <- gemm_packed            gemm.hpp:27-28 (gemm.cpp:170-219)
+ *   fpx_effective_scale <- effective_scale      codec.hpp:76   (codec.cpp:195-199)
+ *   fpx_format_check / fpx_split_for_format / fpx_max_representable
+ *                     <- FpxFormat::make / SplitScheme::for_format /
+ *                        FpxFormat::max_representable  format.hpp:26-57
+ * The C++ value-type wrappers with the reference's exact signatures live in
+ * include/fpx_b200.hpp.
+ *
+ * Conventions
+ *   - Status: 0 on success, otherwise 1 + fpx::ErrorCode (error.hpp:10-24),
+ *     or FPX_ERR_CUDA / FPX_ERR_DEVICE for runtime failures.  Nothing throws
+ *     across this boundary.  fpx_last_error() returns the thread-local
+ *     message of the last failure on the calling thread ("error[<code>] ...",
+ *     error.cpp:24-35).
+ *   - Every device pointer is caller-owned; all work is enqueued on `stream`
+ *     (a cudaStream_t; NULL = legacy default stream).  Calls on distinct
+ *     streams may run concurrently (reference: pure/reentrant).
+ *   - Functions whose reference counterpart throws on data-dependent errors
+ *     (NaN row, scale overflow) synchronise `stream` when `status_dev` is
+ *     NULL and return the error; pass a device status word to stay async.
+ *   - Formats: exp_bits/man_bits as FpxFormat (E 1..5, M 0..6, 3..8 bits).
+ *     The fused linear kernel serves e3m2 and e2m3 ([2,4] split) and e2m2
+ *     ([4,1] split); pack/unpack/dequantize/quantize serve every format.
+ *   - Matrices: weights row-major fp32 or fp16; codes row-major u8 padded to
+ *     multiples of 64; scales one fp16 bit pattern per padded row;
+ *     activations fp16 col-major K x N (= [N][K] row-major); outputs fp32
+ *     col-major (padded rows) x N, leading dimension ldc.
+ */
+#ifndef FPX_C_H_
+#define FPX_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fpx_stream_t; /* == cudaStream_t */
+
+enum fpx_status {
+    FPX_OK = 0,
+    FPX_ERR_INVALID_FORMAT = 1,
+    FPX_ERR_INVALID_CODE = 2,
+    FPX_ERR_INVALID_VALUE = 3,
+    FPX_ERR_SCALE_OVERFLOW = 4,
+    FPX_ERR_SHAPE_MISMATCH = 5,
+    FPX_ERR_RAGGED_INPUT = 6,
+    FPX_ERR_UNSUPPORTED_SPLIT = 7,
+    FPX_ERR_INDEX_OUT_OF_RANGE = 8,
+    FPX_ERR_BAD_MAGIC = 9,
+    FPX_ERR_BAD_VERSION = 10,
+    FPX_ERR_TRUNCATED = 11,
+    FPX_ERR_CORRUPT = 12,
+    FPX_ERR_IO_FAILURE = 13,
+    FPX_ERR_CUDA = 100,   /* CUDA runtime/driver error (message has details) */
+    FPX_ERR_DEVICE = 101  /* no sm_100 device / feature unavailable */
+};
+
+enum fpx_dtype { FPX_FP32 = 0, FPX_FP16 = 1 }; /* codec.hpp:10 Dtype */
+
+/* ---- library / host-only helpers (no GPU needed) ---------------------- */
+const char* fpx_last_error(void);
+const char* fpx_status_name(int status);   /* error.cpp:5-22 names */
+int fpx_version(void);                     /* major*10000 + minor*100 + patch */
+int fpx_format_check(int exp_bits, int man_bits);            /* 0 or FPX_ERR_INVALID_FORMAT */
+int fpx_split_for_format(int exp_bits, int man_bits, int* widths /* [3] */); /* #segments, 0 = none */
+float fpx_max_representable(int exp_bits, int man_bits);
+uint16_t fpx_effective_scale(uint16_t row_scale, int exp_bits, int man_bits);
+uint32_t fpx_pad64(uint32_t n);
+/* Bytes of segment `seg` of a rows_p x cols_p packed matrix (512*w per tile). */
+size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width);
+
+/* ---- K0: quantize (codec.cpp:105-177) --------------------------------
+ * w: rows x cols row-major, dtype FPX_FP32 or FPX_FP16 (device).
+ * codes: pad64(rows) x pad64(cols) bytes; scales: pad64(rows) fp16 patterns.
+ * Errors (first failing row in row order, like the reference):
+ *   FPX_ERR_INVALID_VALUE (NaN in row), FPX_ERR_SCALE_OVERFLOW.
+ * status_dev: optional device uint64 receiving (row << 8 | status) of the
+ * first failing row, or UINT64_MAX; when NULL the call synchronises. */
+int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int exp_bits, int man_bits,
+                 uint8_t* codes, uint16_t* scales, uint64_t* status_dev, fpx_stream_t stream);
+
+/* ---- K1: pre-pack (prepack.cpp:153-209) -------------------------------
+ * codes: rows_p x cols_p (multiples of 64); widths/nseg: the split (NULL ->
+ * the format's preset, format.cpp:59-69); streams[i]: device buffers of
+ * fpx_stream_bytes(rows_p, cols_p, widths[i]).  scales (device) are checked
+ * for a finite effective scale (prepack.cpp:165-168; synchronises). */
+int fpx_prepack(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p,
+                int exp_bits, int man_bits, const int* widths, int nseg, uint8_t* const* streams,
+                fpx_stream_t stream);
+
+/* ---- unpack (prepack.cpp:211-260) ------------------------------------- */
+int fpx_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32_t cols_p, int exp_bits,
+               int man_bits, const int* widths, int nseg, uint8_t* codes, fpx_stream_t stream);
+
+/* ---- K3: de-quantise to fp16 (codec.cpp:179-193, bit-exact) -----------
+ * w_f16: rows_p x cols_p row-major fp16 patterns.  e3m2/e2m3 [2,4] and
+ * e2m2 [4,1] run the fused kernel's register path; other formats a LUT. */
+int fpx_dequantize(const uint8_t* const* streams, int nseg, const int* widths,
+                   const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int exp_bits,
+                   int man_bits, uint16_t* w_f16, fpx_stream_t stream);
+
+/* ---- K2: fused FPx linear (gemm.cpp:170-219) ---------------------------
+ * C(m, j) = sum_k dequant(W)(m, k) * act(k, j): W packed rows_p x cols_p,
+ * act fp16 col-major k_act x n with k_act == cols_p or the original cols
+ * (zero-extended, gemm.cpp:15-30), C fp32 col-major, C(m,j) at
+ * c[j*ldc + m] for m < rows_p (ldc >= rows_p).
+ * split_k: K chunks per 128-row tile; 0 = fpx_linear_default_split().  The
+ * result depends only on (W, act, split_k) -- never on scheduling -- so a
+ * tile-row shard computed with the full problem's split_k is bit-identical
+ * to the same rows of the unsharded result.
+ * workspace: device buffer of >= fpx_linear_workspace_size(...) bytes,
+ * zero-filled once before first use (it self-cleans); may be NULL when the
+ * size is 0. */
+int fpx_linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n);
+size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int split_k);
+int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
+               uint32_t cols_p, int exp_bits, int man_bits, const uint16_t* act, uint32_t k_act, uint32_t n,
+               float* c, uint32_t ldc, int split_k, void* workspace, size_t workspace_bytes,
+               fpx_stream_t stream);
+
+/* ---- multi-GPU helpers (tile-row / output-channel sharding) -----------
+ * Contiguous tile-row range [*tr0, *tr1) of rank `rank` of `world` for a
+ * matrix of rows_p rows (balanced to within one tile-row). */
+void fpx_shard_rows(uint32_t rows_p, int rank, int world, uint32_t* tr0, uint32_t* tr1);
+/* gathered: [world][n][m_slot] fp32 (device, e.g. from ncclAllGather of each
+ * rank's col-major slice padded to m_slot rows); row0/nrows: device arrays
+ * of per-rank first row / row count.  Writes col-major c (ldc). */
+int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32_t* nrows, int world,
+                       uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream);
+
+/* ---- debug ------------------------------------------------------------
+ * With FPX_LINEAR_TRACE=1 in the environment, every fpx_linear launch records
+ * clock64 stamps of CTA 0's pipeline events (7 events x 512 stages, row-major)
+ * which this call copies to host (synchronous). */
+int fpx_debug_trace(uint64_t* host, size_t words);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FPX_C_H_ */

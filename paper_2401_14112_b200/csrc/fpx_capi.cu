@@ -1,0 +1,404 @@
+// fpx_capi.cu -- implementation of the C-ABI in include/fpx_c.h: argument
+// validation with the reference's error codes/messages, tensor-map encoding,
+// workspace carving, and dispatch to the sm_100a kernels.  No exception and
+// no host compute fallback: if the device or a kernel is unavailable the
+// call fails with FPX_ERR_DEVICE / FPX_ERR_CUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/fpx_c.h"
+#include "fpx_kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+const char* kNames[] = {"ok",            "invalid-format", "invalid-code",       "invalid-value",
+                        "scale-overflow", "shape-mismatch", "ragged-input",       "unsupported-split",
+                        "index-out-of-range", "bad-magic",   "bad-version",        "truncated",
+                        "corrupt",       "io-failure"};
+
+int fail(int status, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = std::string("error[") + fpx_status_name(status) + "] " + buf;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(FPX_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define FPX_CUDA(call)                                       \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+    } while (0)
+
+int bias_of(int e) { return (1 << (e - 1)) - 1; }
+
+// Device gate: the kernels are sm_100a-only (tcgen05/TMEM/TMA).
+int check_device(bool need_sm100) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(FPX_ERR_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+    if (!need_sm100) return FPX_OK;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(FPX_ERR_DEVICE, "device %d is sm_%d%d; libfpx_b200 kernels are built for sm_100a", dev,
+                    major, minor);
+    return FPX_OK;
+}
+
+int resolve_split(int e, int m, const int* widths, int nseg, int* w_out) {
+    if (widths == nullptr || nseg == 0) {
+        nseg = fpx_split_for_format(e, m, w_out);
+        return nseg;
+    }
+    if (nseg < 1 || nseg > 3) return -1;
+    int tot = 0;
+    for (int i = 0; i < nseg; ++i) {
+        if (widths[i] != 1 && widths[i] != 2 && widths[i] != 4) return -1;
+        w_out[i] = widths[i];
+        tot += widths[i];
+    }
+    return tot == 1 + e + m ? nseg : -1;
+}
+
+int num_sms() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+uint32_t npad_of(uint32_t n) {
+    uint32_t p = 16;
+    while (p < n) p *= 2;
+    return p;
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+constexpr size_t kLinearCounterBytes = 64 * 1024;  // split-K arrival counters (4 per 128-row tile)
+
+// Debug-only pipeline trace (FPX_LINEAR_TRACE=1): device buffer of
+// kTraceWords clock64 stamps written by CTA 0 of fpx_linear.
+constexpr size_t kTraceWords = 16 * 512;
+unsigned long long* g_trace = nullptr;
+unsigned long long* debug_trace_buffer() {
+    static bool enabled = [] {
+        const char* e = std::getenv("FPX_LINEAR_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!enabled) return nullptr;
+    if (!g_trace && cudaMalloc(&g_trace, kTraceWords * sizeof(unsigned long long)) != cudaSuccess) g_trace = nullptr;
+    if (g_trace) cudaMemset(g_trace, 0, kTraceWords * sizeof(unsigned long long));
+    return g_trace;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fpx_last_error(void) { return g_last_error.c_str(); }
+
+const char* fpx_status_name(int s) {
+    if (s >= 0 && s <= 13) return kNames[s];
+    if (s == FPX_ERR_CUDA) return "cuda";
+    if (s == FPX_ERR_DEVICE) return "device";
+    return "unknown";
+}
+
+int fpx_version(void) { return 100; }
+
+int fpx_format_check(int e, int m) {
+    const int t = 1 + e + m;
+    if (e < 1 || e > 5 || m < 0 || m > 6 || t < 3 || t > 8)
+        return fail(FPX_ERR_INVALID_FORMAT, "unsupported minifloat format e%dm%d", e, m);
+    return FPX_OK;
+}
+
+int fpx_split_for_format(int e, int m, int* widths) {
+    static const int kW[9][3] = {{0}, {0}, {0}, {2, 1}, {4}, {4, 1}, {2, 4}, {4, 2, 1}, {4, 4}};
+    static const int kN[9] = {0, 0, 0, 2, 1, 2, 2, 3, 2};
+    const int t = 1 + e + m;
+    if (t < 3 || t > 8) return 0;
+    for (int i = 0; i < kN[t]; ++i) widths[i] = kW[t][i];
+    return kN[t];
+}
+
+float fpx_max_representable(int e, int m) {
+    const double frac = 2.0 - std::ldexp(1.0, -m);
+    return static_cast<float>(std::ldexp(frac, ((1 << e) - 1) - bias_of(e)));
+}
+
+uint16_t fpx_effective_scale(uint16_t s, int e, int m) {
+    (void)m;
+    // fp16 -> fp32 exact, * 2^(15-bias) exact, fp32 -> fp16 RNE
+    uint32_t sign = (s >> 15) & 1u, ex = (s >> 10) & 31u, man = s & 1023u;
+    float v = ex == 0 ? std::ldexp(float(man), -24) : (ex == 31 ? INFINITY : std::ldexp(float(1024 + man), int(ex) - 25));
+    if (ex == 31 && man) v = NAN;
+    if (sign) v = -v;
+    const float r = v * std::ldexp(1.0f, 15 - bias_of(e));
+    // float -> half RNE via the hardware-independent path
+    uint32_t x;
+    std::memcpy(&x, &r, 4);
+    const uint16_t hs = static_cast<uint16_t>((x >> 16) & 0x8000u);
+    const uint32_t a = x & 0x7fffffffu;
+    if (a >= 0x7f800000u) return a > 0x7f800000u ? uint16_t(hs | 0x7e00u | ((a & 0x7fffffu) >> 13)) : uint16_t(hs | 0x7c00u);
+    const int e16 = int(a >> 23) - 112;
+    if (e16 >= 31) return hs | 0x7c00u;
+    const uint32_t sig = (a & 0x7fffffu) | 0x800000u;
+    int drop;
+    uint32_t base;
+    if (e16 >= 1) {
+        drop = 13;
+        base = (uint32_t(e16) << 10) | ((sig >> 13) & 0x3ffu);
+    } else {
+        if (e16 < -10) return hs;
+        drop = 14 - e16;
+        base = sig >> drop;
+    }
+    const uint32_t rem = sig & ((1u << drop) - 1u), halfway = 1u << (drop - 1);
+    if (rem > halfway || (rem == halfway && (base & 1u))) ++base;
+    return static_cast<uint16_t>(hs | base);
+}
+
+uint32_t fpx_pad64(uint32_t n) { return (n + 63u) / 64u * 64u; }
+
+size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width) {
+    return static_cast<size_t>(rows_p / 64u) * (cols_p / 64u) * 512u * static_cast<size_t>(width);
+}
+
+// ---------------------------------------------------------------- K0
+int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, int m, uint8_t* codes,
+                 uint16_t* scales, uint64_t* status_dev, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (dtype != FPX_FP32 && dtype != FPX_FP16)
+        return fail(FPX_ERR_INVALID_VALUE, "quantize expects a row-major fp32 matrix");
+    if (rows == 0 || cols == 0) return fail(FPX_ERR_SHAPE_MISMATCH, "empty matrix");
+    if (!w || !codes || !scales) return fail(FPX_ERR_INVALID_VALUE, "null buffer");
+    if (int st = check_device(false)) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
+    bool own = false;
+    if (!status) {
+        FPX_CUDA(cudaMallocAsync(&status, sizeof(unsigned long long), s));
+        own = true;
+    }
+    FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    const double maxrep = static_cast<double>(fpx_max_representable(e, m));
+    FPX_CUDA(launch_quantize(w, dtype, rows, cols, fpx_pad64(rows), fpx_pad64(cols), e, m, maxrep, codes, scales,
+                             status, s));
+    if (!own) return FPX_OK;
+    unsigned long long host = 0;
+    FPX_CUDA(cudaMemcpyAsync(&host, status, sizeof host, cudaMemcpyDeviceToHost, s));
+    FPX_CUDA(cudaFreeAsync(status, s));
+    FPX_CUDA(cudaStreamSynchronize(s));
+    if (host == ~0ull) return FPX_OK;
+    const unsigned long long row = host >> 8;
+    const int code = static_cast<int>(host & 0xffu);
+    if (code == FPX_ERR_INVALID_VALUE) return fail(code, "row %llu contains NaN", row);
+    return fail(code, "row %llu scale does not fit in fp16 (or its 2^%d-folded effective scale overflows)", row,
+                15 - bias_of(e));
+}
+
+// ---------------------------------------------------------------- K1
+int fpx_prepack(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int e, int m,
+                const int* widths, int nseg, uint8_t* const* streams, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (rows_p == 0 || cols_p == 0 || rows_p % 64 || cols_p % 64)
+        return fail(FPX_ERR_SHAPE_MISMATCH,
+                    "matrix dims must be padded to multiples of 64 at quantize time before packing");
+    int w[3];
+    const int ns = resolve_split(e, m, widths, nseg, w);
+    if (ns <= 0) return fail(FPX_ERR_UNSUPPORTED_SPLIT, "split widths do not cover e%dm%d", e, m);
+    if (int st = check_device(false)) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (scales) {
+        unsigned int* bad = nullptr;
+        FPX_CUDA(cudaMallocAsync(&bad, sizeof(unsigned int), s));
+        FPX_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned int), s));
+        FPX_CUDA(launch_check_scales(scales, rows_p, 15 - bias_of(e), bad, s));
+        unsigned int hb = 0;
+        FPX_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
+        FPX_CUDA(cudaFreeAsync(bad, s));
+        FPX_CUDA(cudaStreamSynchronize(s));
+        if (hb) return fail(FPX_ERR_SCALE_OVERFLOW, "effective scale overflows fp16");
+    }
+    FPX_CUDA(launch_prepack(codes, rows_p, cols_p, 1 + e + m, ns, w, streams, s));
+    return FPX_OK;
+}
+
+int fpx_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32_t cols_p, int e, int m, const int* widths,
+               int nseg, uint8_t* codes, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (rows_p == 0 || cols_p == 0 || rows_p % 64 || cols_p % 64)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "packed dims must be multiples of 64");
+    int w[3];
+    const int ns = resolve_split(e, m, widths, nseg, w);
+    if (ns <= 0) return fail(FPX_ERR_UNSUPPORTED_SPLIT, "split widths do not cover e%dm%d", e, m);
+    if (int st = check_device(false)) return st;
+    FPX_CUDA(launch_unpack(streams, rows_p, cols_p, 1 + e + m, ns, w, codes, reinterpret_cast<cudaStream_t>(stream)));
+    return FPX_OK;
+}
+
+// ---------------------------------------------------------------- K3
+int fpx_dequantize(const uint8_t* const* streams, int nseg, const int* widths, const uint16_t* scales,
+                   uint32_t rows_p, uint32_t cols_p, int e, int m, uint16_t* w_f16, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (rows_p == 0 || cols_p == 0 || rows_p % 64 || cols_p % 64)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "packed dims must be multiples of 64");
+    int w[3];
+    const int ns = resolve_split(e, m, widths, nseg, w);
+    if (ns <= 0) return fail(FPX_ERR_UNSUPPORTED_SPLIT, "split widths do not cover e%dm%d", e, m);
+    if (int st = check_device(false)) return st;
+    // FPX_DEQUANT_PATH = cvt (default, the fused kernel's path) | swar | lut
+    const char* pe = std::getenv("FPX_DEQUANT_PATH");
+    const int path = !pe ? 0 : (pe[0] == 's' ? 1 : (pe[0] == 'l' ? 2 : 0));
+    FPX_CUDA(launch_dequant(streams, ns, w, scales, rows_p, cols_p, e, m, w_f16, path,
+                            reinterpret_cast<cudaStream_t>(stream)));
+    return FPX_OK;
+}
+
+// ---------------------------------------------------------------- K2
+int fpx_linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n) {
+    return linear_default_split(rows_p, cols_p, n < 256 ? n : 256, num_sms());
+}
+
+// The kernel reads activations through a 3-D tensor map {64, n, K/64} whose
+// k-tile stride is 64 elements, so it needs rows of exactly cols_p (padded K)
+// elements, 16-byte aligned.  Anything else (K_act < cols_p, i.e. the
+// reference's zero-extension of b beyond b.rows, gemm.cpp:15-18, or an
+// unaligned pointer) is first staged into a zero-padded [n][cols_p] buffer.
+static bool act_needs_stage(const uint16_t* act, uint32_t k_act, uint32_t cols_p) {
+    return k_act != cols_p || (reinterpret_cast<uintptr_t>(act) % 16u) != 0;
+}
+
+// Workspace layout: [split-K arrival counters, kLinearCounterBytes, always at
+// offset 0 so they stay valid (self-cleaning) across calls of any shape]
+// [fp32 split-K partials][staged activations].
+struct WsLayout {
+    size_t part_off, stage_off, total;
+};
+
+static WsLayout ws_layout(uint32_t rows_p, uint32_t cols_p, uint32_t n, int split_k, bool stage) {
+    const uint32_t nb = n < 256 ? n : 256;
+    WsLayout l;
+    l.part_off = kLinearCounterBytes;
+    l.stage_off = l.part_off + align256(linear_workspace_bytes(rows_p, nb, split_k));
+    l.total = l.stage_off + (stage ? align256(static_cast<size_t>(cols_p) * n * sizeof(uint16_t)) : 0);
+    return l;
+}
+
+size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int split_k) {
+    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
+    // A 16-byte-misaligned activation pointer also needs the staging area;
+    // callers passing such pointers should size with k_act != cols_p.
+    return ws_layout(rows_p, cols_p, n, split_k, k_act != cols_p).total;
+}
+
+int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p,
+               int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, float* c, uint32_t ldc, int split_k,
+               void* workspace, size_t workspace_bytes, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    int fmt = -1;
+    int w[3];
+    const int ns = resolve_split(e, m, nullptr, 0, w);
+    if (e == 3 && m == 2) fmt = 0;
+    else if (e == 2 && m == 3) fmt = 1;
+    else if (e == 2 && m == 2) fmt = 2;
+    if (fmt < 0 || nseg != ns)
+        return fail(FPX_ERR_UNSUPPORTED_SPLIT, "fused linear serves e3m2/e2m3 ([2,4]) and e2m2 ([4,1]); got e%dm%d", e,
+                    m);
+    if (rows_p == 0 || cols_p == 0 || rows_p % 64 || cols_p % 64)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "packed dims must be multiples of 64");
+    if (k_act == 0 || k_act > cols_p)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "weight cols %u do not match activation rows %u", cols_p, k_act);
+    if (ldc < rows_p) return fail(FPX_ERR_SHAPE_MISMATCH, "ldc %u < rows %u", ldc, rows_p);
+    if (n == 0) return FPX_OK;
+    if (int st = check_device(true)) return st;
+    const int kt = static_cast<int>(cols_p / 64);
+    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
+    if (split_k > kt) split_k = kt;
+    if (split_k > 1 && (rows_p + 127) / 128 * 4 * sizeof(uint32_t) > kLinearCounterBytes)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "rows %u exceed the split-K counter table", rows_p);
+    const bool stage = act_needs_stage(act, k_act, cols_p);
+    const WsLayout lay = ws_layout(rows_p, cols_p, n, split_k, stage);
+    if (workspace == nullptr || workspace_bytes < lay.total)
+        return fail(FPX_ERR_INVALID_VALUE, "workspace of %zu bytes required (got %zu)", lay.total, workspace_bytes);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    const uint16_t* a = act;
+    if (stage) {
+        uint16_t* staged = reinterpret_cast<uint16_t*>(ws + lay.stage_off);
+        FPX_CUDA(launch_stage_act(act, k_act, n, cols_p, staged, s));
+        a = staged;
+    }
+    uint32_t* counters = reinterpret_cast<uint32_t*>(ws);
+    float* part = reinterpret_cast<float*>(ws + lay.part_off);
+    const char* g = std::getenv("FPX_LINEAR_GRID");
+    const int grid = g ? std::atoi(g) : num_sms();
+    for (uint32_t n0 = 0; n0 < n; n0 += 256) {
+        LinearLaunch L{};
+        L.fmt = fmt;
+        L.s_hi = streams[0];
+        L.s_lo = streams[1];
+        L.scales = scales;
+        L.rows_p = rows_p;
+        L.cols_p = cols_p;
+        L.act = a + static_cast<size_t>(n0) * cols_p;
+        L.lda = cols_p;
+        L.n = (n - n0) < 256 ? (n - n0) : 256;
+        L.c = c + static_cast<size_t>(n0) * ldc;
+        L.ldc = ldc;
+        L.split = split_k;
+        L.ws = part;
+        L.counters = counters;
+        L.grid = grid;
+        L.trace = debug_trace_buffer();
+        const cudaError_t err = launch_linear(L, s);
+        if (err == cudaErrorNotSupported) return fail(FPX_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+        if (err != cudaSuccess) return cuda_fail(err, "fpx_linear_kernel launch");
+    }
+    return FPX_OK;
+}
+
+// ---------------------------------------------------------------- multi-GPU
+int fpx_debug_trace(uint64_t* host, size_t words) {
+    if (!g_trace) return fail(FPX_ERR_INVALID_VALUE, "no trace recorded (set FPX_LINEAR_TRACE=1)");
+    if (words > kTraceWords) words = kTraceWords;
+    FPX_CUDA(cudaMemcpy(host, g_trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return FPX_OK;
+}
+
+void fpx_shard_rows(uint32_t rows_p, int rank, int world, uint32_t* tr0, uint32_t* tr1) {
+    const uint64_t trs = rows_p / 64u;
+    if (world <= 0) world = 1;
+    *tr0 = static_cast<uint32_t>(trs * rank / world);
+    *tr1 = static_cast<uint32_t>(trs * (rank + 1) / world);
+}
+
+int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32_t* nrows, int world, uint32_t m_slot,
+                       uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream) {
+    if (world <= 0) return fail(FPX_ERR_INVALID_VALUE, "world must be positive");
+    if (int st = check_device(false)) return st;
+    FPX_CUDA(launch_gather_permute(gathered, row0, nrows, world, m_slot, n, c, ldc,
+                                   reinterpret_cast<cudaStream_t>(stream)));
+    return FPX_OK;
+}
+
+}  // extern "C"

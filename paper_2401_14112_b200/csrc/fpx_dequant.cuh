@@ -1,0 +1,224 @@
+// fpx_dequant.cuh -- register-level de-quantisation of the packed FPx
+// streams into fp16 mma A-fragments.  Shared by the fused linear kernel
+// (fpx_linear.cu) and the bit-exact verification kernel (fpx_codec.cu), so
+// the dequant bits the GEMM consumes are exactly the bits the parity tests
+// compare against the reference's dequantize_reference (codec.cpp:179-193).
+//
+// Packed layout (reference prepack.cpp:29-134): per 64x64
+// tile, per segment width w, thread t's word j lives at byte (j*32+t)*4 of
+// the tile's 512*w-byte block; code k of thread t sits in iteration k/4,
+// byte lane {1,3,0,2}[k%4], group (k/4) % (8/w) of word (k/4)/(8/w), at bits
+// [8*lane+8-w*(g+1), 8*lane+8-w*g).
+//
+// A warp of the linear kernel owns 32 rows of a 64-row tile: half h (0/1)
+// covers chunks 2h and 2h+1 of every slice, i.e. iterations i = 4h+j,
+// j = 0..3, of the reference's 8-iteration loop (simt.cpp:21-42).  For one
+// slice s the thread needs:
+//   [2,4] split (FP6 e3m2/e2m3): 2-bit word 2s+h, 4-bit words 4s+2h, 4s+2h+1
+//   [4,1] split (FP5 e2m2)     : 4-bit words 4s+2h, 4s+2h+1, 1-bit word s
+// and produces, per j, R1 (pair rows 16c+t/4) and R2 (rows 16c+8+t/4),
+// c = 2h + j/2, each an f16x2 register in mma A-fragment order.
+//
+// Two register paths, both bit-exact with the reference oracle:
+//  * kHwCvt (default, B200-native): stitch the four codes of iteration j into
+//    the low 6 bits of each byte lane (one LOP3 + shifts), pair the byte
+//    lanes with one PRMT ({1,3} -> R1, {0,2} -> R2, matching the reference's
+//    lane permutation prepack.cpp:17), convert with the sm_100a hardware
+//    FP6 -> f16x2 unpack (cvt.rn.f16x2.e3m2x2 / e2m3x2, SASS F2FP ... UNPACK_B,
+//    which ignores bits 7:6 of each byte) and multiply by the RAW fp16 row
+//    scale.  cvt yields fp16(decode(code)) exactly, so the product is the
+//    oracle's half_mul(float_to_half(decode), scale) by definition.  FP5
+//    e2m2 codes become e2m3 codes by appending a zero mantissa bit (same
+//    bias, exactly representable).  ALU work ~2.5x below the SWAR path and
+//    the converts issue outside the ALU pipe.
+//  * kSwar: the paper's Algorithm 1 (simt.hpp:26-45, simt.cpp:13-44) --
+//    stitch, bias-deferred 4-way cast into fp16 top bits, multiply by the
+//    effective scale fp16(s * 2^(15-bias)) (codec.cpp:195-199).
+#pragma once
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "ptx_sm100.cuh"
+
+namespace fpxk {
+
+enum FmtId : int { kE3M2 = 0, kE2M3 = 1, kE2M2 = 2 };
+enum DqPath : int { kHwCvt = 0, kSwar = 1 };
+
+template <int F>
+struct FmtTraits;
+
+// e3m2: S|EEE|MM, bias 3.
+template <>
+struct FmtTraits<kE3M2> {
+    static constexpr int kBitsHi = 2, kBitsLo = 4;  // stream widths (hi first)
+    static constexpr int kRebias = 12;              // 15 - bias (SWAR path)
+};
+// e2m3: S|EE|MMM, bias 1.
+template <>
+struct FmtTraits<kE2M3> {
+    static constexpr int kBitsHi = 2, kBitsLo = 4;
+    static constexpr int kRebias = 14;
+};
+// e2m2: S|EE|MM, bias 1, split [4,1].
+template <>
+struct FmtTraits<kE2M2> {
+    static constexpr int kBitsHi = 4, kBitsLo = 1;
+    static constexpr int kRebias = 14;
+};
+
+FPX_DEV uint32_t lop3_sel(uint32_t mask_src, uint32_t other, uint32_t mask) {
+    // (mask_src & mask) | (other & ~mask) as one LOP3
+    return (mask_src & mask) | (other & ~mask);
+}
+
+FPX_DEV uint32_t prmt(uint32_t a, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(a), "r"(sel));
+    return d;
+}
+
+// Hardware FP6x2 -> f16x2 (exact).  F = kE3M2 uses e3m2, else e2m3.
+template <int F>
+FPX_DEV void cvt_pairs(uint32_t paired, uint32_t& lo, uint32_t& hi) {
+    if constexpr (F == kE3M2) {
+        asm("{\n\t.reg .b16 l, h;\n\t"
+            "mov.b32 {l, h}, %2;\n\t"
+            "cvt.rn.f16x2.e3m2x2 %0, l;\n\t"
+            "cvt.rn.f16x2.e3m2x2 %1, h;\n\t}"
+            : "=r"(lo), "=r"(hi)
+            : "r"(paired));
+    } else {
+        asm("{\n\t.reg .b16 l, h;\n\t"
+            "mov.b32 {l, h}, %2;\n\t"
+            "cvt.rn.f16x2.e2m3x2 %0, l;\n\t"
+            "cvt.rn.f16x2.e2m3x2 %1, h;\n\t}"
+            : "=r"(lo), "=r"(hi)
+            : "r"(paired));
+    }
+}
+
+// ------------------------------------------------------------ kHwCvt path
+// Codes of iteration j in bits [5:0] of each byte lane (bits 7:6 junk).
+template <int F>
+FPX_DEV void codes_low6(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (&c)[4]) {
+    if constexpr (FmtTraits<F>::kBitsHi == 2) {
+        // 2-bit group j (bits 7-2j..6-2j) -> bits 5:4; 4-bit group j%2 -> bits 3:0
+        c[0] = lop3_sel(wa >> 2, wb >> 4, 0x30303030u);
+        c[1] = lop3_sel(wa, wb, 0x30303030u);
+        c[2] = lop3_sel(wa << 2, wc >> 4, 0x30303030u);
+        c[3] = lop3_sel(wa << 4, wc, 0x30303030u);
+    } else {
+        // e2m2 [4,1] -> e2m3 code (c << 1): 4-bit group j%2 (S E1 E0 M1) -> bits 5:2,
+        // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0.
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t w4 = j < 2 ? wa : wb;
+            const uint32_t hi = (j & 1) ? (w4 << 2) : (w4 >> 2);
+            const int g = 4 * h + j;
+            const uint32_t lo = (g <= 6) ? (wc >> (6 - g)) : (wc << 1);
+            c[j] = (hi & 0x3c3c3c3cu) | (lo & 0x02020202u);
+        }
+    }
+}
+
+// ------------------------------------------------------------ kSwar path
+// Reference stitch_step with the register advance of simt.cpp:25-32 folded
+// into constant shifts: four codes left-aligned at bit 7 of each byte.
+template <int F>
+FPX_DEV uint32_t stitch_hi(uint32_t wa, uint32_t wb, uint32_t wc, int j, int h) {
+    if constexpr (FmtTraits<F>::kBitsHi == 2) {
+        (void)h;
+        const uint32_t f1 = wa << (2 * j);
+        const uint32_t f2 = (j < 2 ? wb : wc) << (4 * (j & 1));
+        return (f1 & 0xc0c0c0c0u) | ((f2 & 0xf0f0f0f0u) >> 2);
+    } else {
+        const uint32_t hi = ((j < 2 ? wa : wb) << (4 * (j & 1))) & 0xf0f0f0f0u;
+        const int g = 4 * h + j;
+        return hi | (((wc << g) & 0x80808080u) >> 4);
+    }
+}
+
+// Bias-deferred cast (Eq. 3): R1 = lanes {1 lo, 3 hi}, R2 = lanes {0, 2}.
+template <int F>
+FPX_DEV void swar_to_half2(uint32_t x, uint32_t& r1, uint32_t& r2) {
+    if constexpr (F == kE3M2) {
+        // reference dequant4 (simt.hpp:40-45)
+        const uint32_t v = (x & 0x80808080u) | ((x >> 2) & 0x1f1f1f1fu);
+        r1 = v & 0x9f009f00u;
+        r2 = (v & 0x009f009fu) << 8;
+    } else if constexpr (F == kE2M3) {
+        r1 = (x & 0x80008000u) | ((x >> 3) & 0x0f800f80u);
+        const uint32_t y = x << 8;
+        r2 = (y & 0x80008000u) | ((y >> 3) & 0x0f800f80u);
+    } else {
+        r1 = (x & 0x80008000u) | ((x >> 3) & 0x0f000f00u);
+        const uint32_t y = x << 8;
+        r2 = (y & 0x80008000u) | ((y >> 3) & 0x0f000f00u);
+    }
+}
+
+// One slice of one half-warp-tile: 4 iterations -> {R1, R2} per j, already
+// multiplied (fp16 RNE) by the row scales.  sc[lc][0] = scale (both halves)
+// of row 16(2h+lc)+t/4, sc[lc][1] of +8: RAW scales for kHwCvt, effective
+// scales for kSwar (see row_scale_for).
+template <int F, int P = kHwCvt>
+FPX_DEV void dequant_slice_half(uint32_t wa, uint32_t wb, uint32_t wc, int h, const uint32_t (&sc)[2][2],
+                                uint32_t (&r1)[4], uint32_t (&r2)[4]) {
+    if constexpr (P == kHwCvt) {
+        uint32_t c[4];
+        codes_low6<F>(wa, wb, wc, h, c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t a, b;
+            cvt_pairs<F == kE3M2 ? kE3M2 : kE2M3>(prmt(c[j], 0x2031u), a, b);
+            r1[j] = hmul2_rn(a, sc[j >> 1][0]);
+            r2[j] = hmul2_rn(b, sc[j >> 1][1]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t a, b;
+            swar_to_half2<F>(stitch_hi<F>(wa, wb, wc, j, h), a, b);
+            r1[j] = hmul2_rn(a, sc[j >> 1][0]);
+            r2[j] = hmul2_rn(b, sc[j >> 1][1]);
+        }
+    }
+}
+
+// Byte offsets (within a tile's stream block) of the three words one thread
+// needs for slice s, half h: {wa, wb, wc} per the table at the top.
+template <int F>
+FPX_DEV void slice_word_offsets(int s, int h, uint32_t t, uint32_t& oa, uint32_t& ob, uint32_t& oc, bool& a_in_hi,
+                                bool& b_in_hi, bool& c_in_hi) {
+    if constexpr (FmtTraits<F>::kBitsHi == 2) {
+        oa = ((2 * s + h) * 32 + t) * 4;          // 2-bit stream
+        ob = ((4 * s + 2 * h) * 32 + t) * 4;      // 4-bit stream
+        oc = ((4 * s + 2 * h + 1) * 32 + t) * 4;  // 4-bit stream
+        a_in_hi = true, b_in_hi = false, c_in_hi = false;
+    } else {
+        oa = ((4 * s + 2 * h) * 32 + t) * 4;      // 4-bit stream (hi)
+        ob = ((4 * s + 2 * h + 1) * 32 + t) * 4;  // 4-bit stream (hi)
+        oc = (s * 32 + t) * 4;                    // 1-bit stream (lo)
+        a_in_hi = true, b_in_hi = true, c_in_hi = false;
+    }
+}
+
+// fp16 bits -> fp16 bits, fp16(x * 2^k) computed exactly in fp32 then RNE
+// (codec.cpp:195-199 effective_scale).
+FPX_DEV uint16_t effective_scale_dev(uint16_t s, int rebias) {
+    const float v = __half2float(__ushort_as_half(s)) * __int_as_float((127 + rebias) << 23);
+    return __half_as_ushort(__float2half_rn(v));
+}
+
+FPX_DEV uint32_t bcast_half2(uint16_t h) { return static_cast<uint32_t>(h) * 0x10001u; }
+
+// The per-row multiplier a path expects, broadcast to both halves.
+template <int F, int P = kHwCvt>
+FPX_DEV uint32_t row_scale_for(uint16_t raw) {
+    if constexpr (P == kHwCvt) return bcast_half2(raw);
+    else return bcast_half2(effective_scale_dev(raw, FmtTraits<F>::kRebias));
+}
+
+}  // namespace fpxk

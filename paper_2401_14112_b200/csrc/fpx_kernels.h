@@ -1,0 +1,48 @@
+// fpx_kernels.h -- host-side launch entry points of the sm_100a kernels
+// (internal to libfpx_b200.so; the public surface is include/fpx_c.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+cudaError_t launch_quantize(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
+                            uint32_t cols_p, int e, int m, double maxrep, uint8_t* codes,
+                            uint16_t* scales, unsigned long long* status, cudaStream_t st);
+cudaError_t launch_prepack(const uint8_t* codes, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,
+                           const int* widths, uint8_t* const* streams, cudaStream_t st);
+cudaError_t launch_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,
+                          const int* widths, uint8_t* codes, cudaStream_t st);
+cudaError_t launch_dequant(const uint8_t* const* streams, int nseg, const int* widths, const uint16_t* scales,
+                           uint32_t rows_p, uint32_t cols_p, int e, int m, uint16_t* out, int path,
+                           cudaStream_t st);
+cudaError_t launch_check_scales(const uint16_t* scales, uint32_t n, int rebias, unsigned int* bad,
+                                cudaStream_t st);
+cudaError_t launch_stage_act(const uint16_t* src, uint32_t k_act, uint32_t n, uint32_t k_pad, uint16_t* dst,
+                             cudaStream_t st);
+cudaError_t launch_gather_permute(const float* g, const uint32_t* row0, const uint32_t* nrows, int world,
+                                  uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, cudaStream_t st);
+
+// Fused de-quantise + tcgen05 GEMM (fpx_linear.cu).
+struct LinearLaunch {
+    int fmt;                   // fpxk::FmtId
+    const uint8_t* s_hi;       // stream of the high segment
+    const uint8_t* s_lo;       // stream of the low segment
+    const uint16_t* scales;    // raw fp16 row scales (rows_p)
+    uint32_t rows_p, cols_p;   // padded weight dims (multiples of 64)
+    const uint16_t* act;       // col-major activations, row j at act + j*lda, K == cols_p
+    uint32_t lda;              // >= cols_p, multiple of 8
+    uint32_t n;                // batch (1..256)
+    float* c;                  // col-major output, element (m, j) at c[j*ldc + m]
+    uint32_t ldc;
+    int split;                 // K chunks per 128-row tile (>= 1)
+    float* ws;                 // split > 1: partial sums
+    uint32_t* counters;        // split > 1: per (tile, quarter) arrival counters (zeroed once)
+    int grid;                  // persistent CTAs (0 = auto)
+    unsigned long long* trace; // debug: per-stage clock64 trace of CTA 0 (7 events x 512 stages), or null
+};
+
+cudaError_t launch_linear(const LinearLaunch& p, cudaStream_t st);
+size_t linear_workspace_bytes(uint32_t rows_p, uint32_t n, int split);
+int linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n, int num_sms);

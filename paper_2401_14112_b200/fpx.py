@@ -1,0 +1,335 @@
+"""Host-side mirror of the reference's FPx API over the B200 C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++
+library (/root/reference/proj/include/fpx/), with device tensors instead of
+host std::vectors:
+
+    reference (namespace fpx)                 here
+    --------------------------------------    -------------------------------
+    FpxFormat / SplitScheme (format.hpp)      FpxFormat / SplitScheme
+    Error / ErrorCode (error.hpp)             FpxError / ErrorCode
+    quantize_matrix (codec.hpp:66)            quantize_matrix    -> K0 kernel
+    dequantize_reference (codec.hpp:72)       dequantize         -> K3 kernel
+    effective_scale (codec.hpp:76)            effective_scale
+    pack / unpack (prepack.hpp:84-86)         pack / unpack      -> K1 kernel
+    gemm_packed (gemm.hpp:27-28)              gemm_packed        -> K2 kernel
+                                              fp6_linear (torch-layout alias)
+
+Matrices follow the reference layouts: weights row-major [rows, cols];
+activations B col-major K x N, which is a contiguous torch tensor of shape
+[N, K]; the result C is fp32 col-major padded-rows x N, i.e. a torch tensor
+of shape [N, rows_p].  torch supplies device memory and streams only; every
+byte of compute runs in libfpx_b200.so's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+
+__all__ = [
+    "ErrorCode", "FpxError", "FpxFormat", "SplitScheme", "QuantizedMatrix", "PackedWeights",
+    "quantize_matrix", "pack", "unpack", "dequantize", "gemm_packed", "fp6_linear", "effective_scale",
+    "linear_workspace", "default_split",
+]
+
+
+class ErrorCode(enum.IntEnum):
+    """error.hpp:10-24 (value = status - 1)."""
+    InvalidFormat = 0
+    InvalidCode = 1
+    InvalidValue = 2
+    ScaleOverflow = 3
+    ShapeMismatch = 4
+    RaggedInput = 5
+    UnsupportedSplit = 6
+    IndexOutOfRange = 7
+    BadMagic = 8
+    BadVersion = 9
+    Truncated = 10
+    Corrupt = 11
+    IoFailure = 12
+
+
+class FpxError(RuntimeError):
+    """fpx::Error (error.hpp:30-44): code + message (+ optional byte offset)."""
+
+    def __init__(self, status: int, message: str, offset: int | None = None):
+        super().__init__(message)
+        self.status = status
+        self.code = ErrorCode(status - 1) if 1 <= status <= 13 else None
+        self.offset = offset
+
+    def formatted(self) -> str:
+        return str(self)
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        L = _lib.load()
+        raise FpxError(status, L.fpx_last_error().decode())
+
+
+@dataclass(frozen=True)
+class FpxFormat:
+    """format.hpp:16-45 -- sign + E + M bits, bias 2^(E-1)-1, no inf/nan."""
+    exp_bits: int = 3
+    man_bits: int = 2
+
+    @property
+    def total_bits(self) -> int:
+        return 1 + self.exp_bits + self.man_bits
+
+    @property
+    def bias(self) -> int:
+        return (1 << (self.exp_bits - 1)) - 1
+
+    def max_representable(self) -> float:
+        return float(_lib.load().fpx_max_representable(self.exp_bits, self.man_bits))
+
+    def name(self) -> str:
+        return f"e{self.exp_bits}m{self.man_bits}"
+
+    @staticmethod
+    def make(exp_bits: int, man_bits: int) -> "FpxFormat":
+        _check(_lib.load().fpx_format_check(exp_bits, man_bits))
+        return FpxFormat(exp_bits, man_bits)
+
+    @staticmethod
+    def parse(name: str) -> "FpxFormat | None":
+        if len(name) != 4 or name[0] != "e" or name[2] != "m" or not name[1].isdigit() or not name[3].isdigit():
+            return None
+        try:
+            return FpxFormat.make(int(name[1]), int(name[3]))
+        except FpxError:
+            return None
+
+    e3m2 = None  # replaced below by constructors (FpxFormat.e3m2())
+
+
+FpxFormat.e3m2 = staticmethod(lambda: FpxFormat(3, 2))  # type: ignore[assignment]
+FpxFormat.e2m3 = staticmethod(lambda: FpxFormat(2, 3))  # type: ignore[attr-defined]
+FpxFormat.e2m2 = staticmethod(lambda: FpxFormat(2, 2))  # type: ignore[attr-defined]
+FpxFormat.e2m1 = staticmethod(lambda: FpxFormat(2, 1))  # type: ignore[attr-defined]
+
+
+@dataclass(frozen=True)
+class SplitScheme:
+    """format.hpp:50-59 -- segment widths, most-significant first."""
+    widths: tuple
+
+    def total(self) -> int:
+        return sum(self.widths)
+
+    @staticmethod
+    def for_format(fmt: FpxFormat) -> "SplitScheme":
+        w = (C.c_int * 3)()
+        n = _lib.load().fpx_split_for_format(fmt.exp_bits, fmt.man_bits, w)
+        if n == 0:
+            raise FpxError(1, f"error[invalid-format] no split for {fmt.name()}")
+        return SplitScheme(tuple(w[i] for i in range(n)))
+
+    @staticmethod
+    def make(widths, fmt: FpxFormat) -> "SplitScheme":
+        widths = tuple(int(x) for x in widths)
+        if any(w not in (1, 2, 4) for w in widths):
+            raise FpxError(7, "error[unsupported-split] segment widths must be 1, 2 or 4")
+        if sum(widths) != fmt.total_bits:
+            raise FpxError(7, f"error[unsupported-split] segment widths must sum to {fmt.total_bits} for {fmt.name()}")
+        return SplitScheme(widths)
+
+
+@dataclass
+class QuantizedMatrix:
+    """codec.hpp:37-51 on device: codes uint8 [rows, cols] (padded to 64), scales fp16 bits [rows]."""
+    format: FpxFormat
+    rows: int
+    cols: int
+    orig_rows: int
+    orig_cols: int
+    codes: torch.Tensor
+    scales: torch.Tensor
+
+
+@dataclass
+class PackedWeights:
+    """prepack.hpp:64-80 on device: one uint8 stream per segment + fp16-bit scales."""
+    format: FpxFormat
+    split: SplitScheme
+    rows: int
+    cols: int
+    orig_rows: int
+    orig_cols: int
+    streams: list = field(default_factory=list)
+    scales: torch.Tensor | None = None
+
+    def tile_rows(self) -> int:
+        return self.rows // 64
+
+    def tile_cols(self) -> int:
+        return self.cols // 64
+
+    @staticmethod
+    def tile_stream_bytes(w: int) -> int:
+        return 512 * w
+
+    def shard(self, tr0: int, tr1: int) -> "PackedWeights":
+        """Tile-rows [tr0, tr1) as zero-copy views (tiles are stored in
+        row-major tile order, prepack.cpp:190-191, so a tile-row range is one
+        contiguous byte range of every stream)."""
+        gc = self.tile_cols()
+        views = [s[tr0 * gc * 512 * w: tr1 * gc * 512 * w] for s, w in zip(self.streams, self.split.widths)]
+        rows = (tr1 - tr0) * 64
+        return PackedWeights(self.format, self.split, rows, self.cols, rows, self.orig_cols, views,
+                             self.scales[tr0 * 64: tr1 * 64])
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def pad64(n: int) -> int:
+    return (n + 63) // 64 * 64
+
+
+def effective_scale(row_scale: int, fmt: FpxFormat) -> int:
+    """codec.cpp:195-199: fp16(scale * 2^(15 - bias))."""
+    return int(_lib.load().fpx_effective_scale(row_scale, fmt.exp_bits, fmt.man_bits))
+
+
+def quantize_matrix(m: torch.Tensor, fmt: FpxFormat) -> QuantizedMatrix:
+    """codec.cpp:105-177: row-wise FPx quantisation on the GPU (bit-exact).
+
+    m: CUDA tensor [rows, cols], fp32 (or fp16: converted exactly, codec.cpp:35-40).
+    Raises FpxError(InvalidValue / ScaleOverflow / ShapeMismatch) like the reference."""
+    L = _lib.load()
+    if m.dim() != 2 or not m.is_cuda:
+        raise FpxError(3, "error[invalid-value] quantize expects a row-major fp32 matrix")
+    if m.dtype == torch.float32:
+        dt = 0
+    elif m.dtype == torch.float16:
+        dt = 1
+    else:
+        raise FpxError(3, "error[invalid-value] quantize expects a row-major fp32 matrix")
+    rows, cols = m.shape
+    if rows == 0 or cols == 0:
+        raise FpxError(5, "error[shape-mismatch] empty matrix")
+    m = m.contiguous()
+    rp, cp = pad64(rows), pad64(cols)
+    codes = torch.empty((rp, cp), dtype=torch.uint8, device=m.device)
+    scales = torch.empty((rp,), dtype=torch.int16, device=m.device)
+    _check(L.fpx_quantize(m.data_ptr(), dt, rows, cols, fmt.exp_bits, fmt.man_bits, codes.data_ptr(),
+                          scales.data_ptr(), None, _stream(m.device)))
+    return QuantizedMatrix(fmt, rp, cp, rows, cols, codes, scales)
+
+
+def pack(q: QuantizedMatrix, split: SplitScheme | None = None) -> PackedWeights:
+    """prepack.cpp:153-209: ahead-of-time bit-level pre-pack (bit-exact bytes)."""
+    L = _lib.load()
+    split = split or SplitScheme.for_format(q.format)
+    dev = q.codes.device
+    streams = [torch.empty(L.fpx_stream_bytes(q.rows, q.cols, w), dtype=torch.uint8, device=dev)
+               for w in split.widths]
+    wid = (C.c_int * len(split.widths))(*split.widths)
+    ptrs = (C.c_void_p * len(streams))(*[s.data_ptr() for s in streams])
+    _check(L.fpx_prepack(q.codes.data_ptr(), q.scales.data_ptr(), q.rows, q.cols, q.format.exp_bits,
+                         q.format.man_bits, wid, len(split.widths), ptrs, _stream(dev)))
+    return PackedWeights(q.format, split, q.rows, q.cols, q.orig_rows or q.rows, q.orig_cols or q.cols, streams,
+                         q.scales.clone())
+
+
+def unpack(p: PackedWeights) -> QuantizedMatrix:
+    """prepack.cpp:211-260: exact inverse of pack."""
+    L = _lib.load()
+    dev = p.streams[0].device
+    codes = torch.empty((p.rows, p.cols), dtype=torch.uint8, device=dev)
+    wid = (C.c_int * len(p.split.widths))(*p.split.widths)
+    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+    _check(L.fpx_unpack(ptrs, p.rows, p.cols, p.format.exp_bits, p.format.man_bits, wid, len(p.split.widths),
+                        codes.data_ptr(), _stream(dev)))
+    return QuantizedMatrix(p.format, p.rows, p.cols, p.orig_rows, p.orig_cols, codes, p.scales.clone())
+
+
+def dequantize(p: PackedWeights) -> torch.Tensor:
+    """fp16 W [rows_p, cols_p] from the packed streams; bit-exact with the
+    reference's dequantize_reference (codec.cpp:179-193)."""
+    L = _lib.load()
+    dev = p.streams[0].device
+    out = torch.empty((p.rows, p.cols), dtype=torch.float16, device=dev)
+    wid = (C.c_int * len(p.split.widths))(*p.split.widths)
+    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+    _check(L.fpx_dequantize(ptrs, len(p.streams), wid, p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                            p.format.man_bits, out.data_ptr(), _stream(dev)))
+    return out
+
+
+_ws_lock = threading.Lock()
+_ws: dict = {}
+
+
+def linear_workspace(device: torch.device, nbytes: int) -> torch.Tensor | None:
+    """Per (device, stream) zero-initialised workspace, grown on demand. Its
+    split-K counter table self-cleans after every launch."""
+    if nbytes == 0:
+        return None
+    key = (device.index if device.index is not None else torch.cuda.current_device(), _stream(device))
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            _ws[key] = buf
+        return buf
+
+
+def default_split(rows_p: int, cols_p: int, n: int) -> int:
+    return int(_lib.load().fpx_linear_default_split(rows_p, cols_p, n))
+
+
+def gemm_packed(p: PackedWeights, b: torch.Tensor, *, out: torch.Tensor | None = None, split_k: int = 0,
+                ldc: int | None = None) -> torch.Tensor:
+    """gemm.cpp:170-219: C = dequant(A) x B on the fused sm_100a kernel.
+
+    b: fp16 activations, col-major K x N == contiguous torch [N, K] with
+       K == p.cols or p.orig_cols (zero-extended, gemm.cpp:15-30).
+    returns C fp32 col-major rows_p x N == torch [N, rows_p] (padded rows kept,
+       like the reference).  `out` may be a preallocated [N, ldc] fp32 tensor.
+    split_k: K chunks per 128-row tile (0 = default); results depend only on
+       (inputs, split_k)."""
+    L = _lib.load()
+    if b.dtype != torch.float16 or b.dim() != 2:
+        raise FpxError(5, "error[shape-mismatch] activations must be fp16 col-major")
+    n, k_act = b.shape
+    if k_act != p.cols and k_act != p.orig_cols:
+        raise FpxError(5, f"error[shape-mismatch] weight cols {p.cols} (orig {p.orig_cols}) do not match "
+                          f"activation rows {k_act}")
+    b = b.contiguous()
+    dev = b.device
+    ldc = ldc or p.rows
+    if out is None:
+        out = torch.empty((n, ldc), dtype=torch.float32, device=dev)
+    if n == 0:
+        return out
+    sk = split_k if split_k > 0 else default_split(p.rows, p.cols, n)
+    misaligned = b.data_ptr() % 16 != 0
+    need = int(L.fpx_linear_workspace_size(p.rows, p.cols, k_act + (1 if misaligned else 0), n, sk))
+    ws = linear_workspace(dev, need)
+    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+    _check(L.fpx_linear(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                        p.format.man_bits, b.data_ptr(), k_act, n, out.data_ptr(), ldc, sk,
+                        _ptr(ws), 0 if ws is None else ws.numel(), _stream(dev)))
+    return out
+
+
+def fp6_linear(act: torch.Tensor, packed: PackedWeights, **kw) -> torch.Tensor:
+    """The paper's fp6_linear(A, packedW, scales) -> C with torch layouts:
+    act [N, K] fp16 -> [N, rows_p] fp32 (scales live in `packed`)."""
+    return gemm_packed(packed, act, **kw)
