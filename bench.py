@@ -75,10 +75,14 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + 5.0
+            while not self.rows and time.time() < t_end:  # sampler is up before timing starts
+                time.sleep(0.01)
+            self.rows.clear()
         except Exception:  # noqa: BLE001
             self.proc = None
         return self
@@ -105,7 +109,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "window": "timed region + 0.3 s of the identical step directly after (nvidia-smi -lms 20)"}
 
 
 def peaks():
@@ -191,6 +196,7 @@ def run_ours(args, rank, world, local):
         cnt = step(cnt)
     nl = len(batches) * args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(cnt + nl)]
+    ev = {i: e for i, e in enumerate(ev)}
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clk:
@@ -200,6 +206,13 @@ def run_ours(args, rank, world, local):
             cnt = step(cnt, ev)
         t1.record(stream)
         barrier()
+        # The timed region lasts a few ms, below nvidia-smi's sampling period:
+        # keep issuing the identical step (untimed) for >= 0.3 s so the
+        # clock/throttle samples describe this workload under load.
+        soak_end = time.time() + 0.3
+        while time.time() < soak_end:
+            cnt = step(cnt)
+            torch.cuda.synchronize(dev)
     total_ms = max_over_ranks(t0.elapsed_time(t1))
     per_launch = np.array([ev[i][0].elapsed_time(ev[i][1]) for i in range(c0, cnt)]) * 1e3  # us
     per_n = {n: float(np.mean(per_launch[j::len(batches)])) for j, n in enumerate(batches)}

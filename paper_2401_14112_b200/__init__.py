@@ -10,5 +10,6 @@ from .fpx import (  # noqa: F401
     ErrorCode, FpxError, FpxFormat, PackedWeights, QuantizedMatrix, SplitScheme, default_split, dequantize,
     effective_scale, fp6_linear, gemm_packed, pack, quantize_matrix, unpack,
 )
+from . import shard  # noqa: F401,E402
 
 __version__ = "0.1.0"
