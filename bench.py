@@ -205,6 +205,7 @@ def run_ours(args, rank, world, local):
         for _ in range(args.steps):
             cnt = step(cnt, ev)
         t1.record(stream)
+        c1 = cnt
         barrier()
         # The timed region lasts a few ms, below nvidia-smi's sampling period:
         # keep issuing the identical step (untimed) for >= 0.3 s so the
@@ -214,7 +215,7 @@ def run_ours(args, rank, world, local):
             cnt = step(cnt)
             torch.cuda.synchronize(dev)
     total_ms = max_over_ranks(t0.elapsed_time(t1))
-    per_launch = np.array([ev[i][0].elapsed_time(ev[i][1]) for i in range(c0, cnt)]) * 1e3  # us
+    per_launch = np.array([ev[i][0].elapsed_time(ev[i][1]) for i in range(c0, c1)]) * 1e3  # us
     per_n = {n: float(np.mean(per_launch[j::len(batches)])) for j, n in enumerate(batches)}
     mean_launch_us = max_over_ranks(float(per_launch.mean()))
 

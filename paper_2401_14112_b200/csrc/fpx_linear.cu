@@ -69,7 +69,8 @@ struct KParams {
     uint32_t ldc;
     uint32_t split;
     uint32_t units;
-    uint32_t dbg;  // bring-up knobs (FPX_LINEAR_DBG): 1 no dequant math, 2 no MMA, 4 no weight loads, 8 no act loads
+    uint32_t dbg;  // bring-up knobs (FPX_LINEAR_DBG): 1 no dequant math, 2 no MMA, 4 no weight loads, 8 no act loads,
+                  // 16 epilogue polls with back-off, 32 dequant A-slot polls with back-off
     unsigned long long* trace;  // optional per-stage clock trace of CTA 0 (fpx_debug_trace), else null
 };
 
@@ -277,7 +278,8 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
             uint32_t mt, ch, k0, k1;
             unit_range(p, u, mt, ch, k0, k1);
             const uint32_t ab = lu % C::kAccBufs, abph = (lu / C::kAccBufs) & 1u;
-            mbar_wait(&accfull[ab], abph);
+            if (p.dbg & 16u) mbar_wait_sleep(&accfull[ab], abph, 256);
+            else mbar_wait(&accfull[ab], abph);
             if (q == 0 && lane == 0) trace_mark(p, kTrEpiFull, lu);
             tc_fence_after();
             const uint32_t m = mt * kTileM + row_l;
@@ -362,7 +364,8 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
                 const uint32_t cnt = min(static_cast<uint32_t>(KS), k1 - k);
                 const uint32_t st = si % C::kStages, ph = (si / C::kStages) & 1u;
                 const uint32_t as = si % C::kAStages, aph = (si / C::kAStages) & 1u;
-                mbar_wait(&aempty[as], aph ^ 1u);
+                if (p.dbg & 32u) mbar_wait_sleep(&aempty[as], aph ^ 1u, 32);
+                else mbar_wait(&aempty[as], aph ^ 1u);
                 if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
                 mbar_wait(&full[st], ph);
                 if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);

@@ -69,6 +69,15 @@ FPX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Polling with back-off, for waiters off the critical path: every
+// try_wait occupies the SM's barrier unit, so idle spinners slow down the
+// latency-critical waiters (MMA issuer, producer) sharing it.
+FPX_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+    }
+}
+
 // ---------------------------------------------------------------- TMA
 FPX_DEV uint64_t policy_evict_first() {
     uint64_t p;
