@@ -145,6 +145,11 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
  * clock64 stamps of CTA 0's pipeline events (7 events x 512 stages, row-major)
  * which this call copies to host (synchronous). */
 int fpx_debug_trace(uint64_t* host, size_t words);
+/* With FPX_LINEAR_TRACE=3: host pointer (mapped, pinned) to 300 x 32 words,
+ * word [cta*32 + warp] = what that warp of the most recent fpx_linear launch
+ * is waiting on (bit 63 set, tag<<56 | stage<<32 | smem_addr<<1 | parity), 0 if
+ * not waiting; NULL otherwise.  For diagnosing a stuck launch. */
+const volatile uint64_t* fpx_debug_progress(void);
 
 #ifdef __cplusplus
 }

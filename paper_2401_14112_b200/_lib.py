@@ -30,10 +30,13 @@ def header_symbols() -> list[str]:
     return sorted(set(re.findall(r"\b(fpx_[a-z0-9_]+)\s*\(", text)))
 
 
-def load(path: str = LIB_PATH) -> C.CDLL:
+def load(path: str | None = None) -> C.CDLL:
+    """Load the in-tree library (FPX_B200_LIB may name an alternate in-tree
+    build, e.g. a tuning variant from `make VARIANT=_x EXTRA=-D...`)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("FPX_B200_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} not built; run `make -C {HERE}` (or __graft_entry__.build())")
     L = C.CDLL(path)
@@ -61,6 +64,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                                  C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
         "fpx_debug_trace": (C.c_int, [C.c_void_p, C.c_size_t]),
+        "fpx_debug_progress": (C.c_void_p, []),
         "fpx_shard_rows": (None, [C.c_uint32, C.c_int, C.c_int, _u32p, _u32p]),
         "fpx_gather_permute": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_uint32, C.c_uint32,
                                          C.c_void_p, C.c_uint32, C.c_void_p]),

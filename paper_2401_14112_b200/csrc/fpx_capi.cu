@@ -93,19 +93,49 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 constexpr size_t kLinearCounterBytes = 64 * 1024;  // split-K arrival counters (4 per 128-row tile)
 
-// Debug-only pipeline trace (FPX_LINEAR_TRACE=1): device buffer of
-// kTraceWords clock64 stamps written by CTA 0 of fpx_linear.
+// Debug-only pipeline trace: device buffer of kTraceWords clock64 /
+// globaltimer stamps written by fpx_linear (CTA 0 per-stage events + a
+// per-CTA timeline).  FPX_LINEAR_TRACE=1: one buffer, cleared per call.
+// FPX_LINEAR_TRACE=2: calls alternate between two buffers that are cleared
+// only on allocation, so two consecutive launches can be compared.
 constexpr size_t kTraceWords = 16 * 512;
 unsigned long long* g_trace = nullptr;
 unsigned long long* debug_trace_buffer() {
-    static bool enabled = [] {
+    static int mode = [] {
         const char* e = std::getenv("FPX_LINEAR_TRACE");
-        return e && e[0] == '1';
+        return e ? std::atoi(e) : 0;
     }();
-    if (!enabled) return nullptr;
-    if (!g_trace && cudaMalloc(&g_trace, kTraceWords * sizeof(unsigned long long)) != cudaSuccess) g_trace = nullptr;
-    if (g_trace) cudaMemset(g_trace, 0, kTraceWords * sizeof(unsigned long long));
-    return g_trace;
+    static unsigned calls = 0;
+    if (mode <= 0 || mode == 3) return nullptr;
+    if (!g_trace) {
+        if (cudaMalloc(&g_trace, 2 * kTraceWords * sizeof(unsigned long long)) != cudaSuccess) return g_trace = nullptr;
+        cudaMemset(g_trace, 0, 2 * kTraceWords * sizeof(unsigned long long));
+    }
+    if (mode == 1) {
+        cudaMemset(g_trace, 0, kTraceWords * sizeof(unsigned long long));
+        return g_trace;
+    }
+    return g_trace + (calls++ & 1u) * kTraceWords;
+}
+
+// FPX_LINEAR_TRACE=3: per (CTA, warp) "currently waiting on" words in mapped
+// host memory (readable by the host while a launch is stuck).
+constexpr size_t kProgWords = 300 * 32;
+unsigned long long* g_prog_host = nullptr;
+volatile unsigned long long* debug_progress_buffer() {
+    static const bool on = [] {
+        const char* e = std::getenv("FPX_LINEAR_TRACE");
+        return e && std::atoi(e) == 3;
+    }();
+    if (!on) return nullptr;
+    if (!g_prog_host) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&g_prog_host), kProgWords * 8, cudaHostAllocMapped) != cudaSuccess)
+            return nullptr;
+        std::memset(g_prog_host, 0, kProgWords * 8);
+    }
+    void* dev = nullptr;
+    if (cudaHostGetDevicePointer(&dev, g_prog_host, 0) != cudaSuccess) return nullptr;
+    return static_cast<volatile unsigned long long*>(dev);
 }
 
 }  // namespace
@@ -370,6 +400,7 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
         L.counters = counters;
         L.grid = grid;
         L.trace = debug_trace_buffer();
+        L.prog = debug_progress_buffer();
         const cudaError_t err = launch_linear(L, s);
         if (err == cudaErrorNotSupported) return fail(FPX_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
         if (err != cudaSuccess) return cuda_fail(err, "fpx_linear_kernel launch");
@@ -378,9 +409,11 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
 }
 
 // ---------------------------------------------------------------- multi-GPU
+const volatile uint64_t* fpx_debug_progress(void) { return reinterpret_cast<const volatile uint64_t*>(g_prog_host); }
+
 int fpx_debug_trace(uint64_t* host, size_t words) {
     if (!g_trace) return fail(FPX_ERR_INVALID_VALUE, "no trace recorded (set FPX_LINEAR_TRACE=1)");
-    if (words > kTraceWords) words = kTraceWords;
+    if (words > 2 * kTraceWords) words = 2 * kTraceWords;
     FPX_CUDA(cudaMemcpy(host, g_trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return FPX_OK;
 }

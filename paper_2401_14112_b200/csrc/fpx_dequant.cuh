@@ -20,10 +20,10 @@
 // c = 2h + j/2, each an f16x2 register in mma A-fragment order.
 //
 // Two register paths, both bit-exact with the reference oracle:
-//  * kHwCvt (default, B200-native): stitch the four codes of iteration j into
-//    the low 6 bits of each byte lane (one LOP3 + shifts), pair the byte
-//    lanes with one PRMT ({1,3} -> R1, {0,2} -> R2, matching the reference's
-//    lane permutation prepack.cpp:17), convert with the sm_100a hardware
+//  * kHwCvt (default, B200-native): pair the byte lanes of each packed word
+//    with one PRMT ({1,3} -> R1, {0,2} -> R2, matching the reference's lane
+//    permutation prepack.cpp:17), stitch the four codes of iteration j into
+//    the low 6 bits of each byte lane (one LOP3 + shifts), convert with the sm_100a hardware
 //    FP6 -> f16x2 unpack (cvt.rn.f16x2.e3m2x2 / e2m3x2, SASS F2FP ... UNPACK_B,
 //    which ignores bits 7:6 of each byte) and multiply by the RAW fp16 row
 //    scale.  cvt yields fp16(decode(code)) exactly, so the product is the
@@ -68,9 +68,13 @@ struct FmtTraits<kE2M2> {
     static constexpr int kRebias = 14;
 };
 
-FPX_DEV uint32_t lop3_sel(uint32_t mask_src, uint32_t other, uint32_t mask) {
-    // (mask_src & mask) | (other & ~mask) as one LOP3
-    return (mask_src & mask) | (other & ~mask);
+// (mask_src & kMask) | (other & ~kMask) as ONE LOP3 (LUT 0xE2 over
+// (a, mask, c)); left to itself nvcc splits it into two.
+template <uint32_t kMask>
+FPX_DEV uint32_t lop3_sel(uint32_t mask_src, uint32_t other) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(d) : "r"(mask_src), "n"(kMask), "r"(other));
+    return d;
 }
 
 FPX_DEV uint32_t prmt(uint32_t a, uint32_t sel) {
@@ -100,24 +104,48 @@ FPX_DEV void cvt_pairs(uint32_t paired, uint32_t& lo, uint32_t& hi) {
 }
 
 // ------------------------------------------------------------ kHwCvt path
-// Codes of iteration j in bits [5:0] of each byte lane (bits 7:6 junk).
+// Right shift on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF).  The
+// ALU pipe (LOP3/SHF/PRMT/F2FP, 16 lanes/clk/SMSP on B200) is what bounds
+// the de-quantiser; HMUL2/IMAD issue to the FMA pipe.  Measured by
+// tests/micro/pipe_bench.cu.
+#ifndef FPX_SHR_ON_FMA
+#define FPX_SHR_ON_FMA 0
+#endif
+template <int K>
+FPX_DEV uint32_t shr(uint32_t x) {
+#if FPX_SHR_ON_FMA
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(1u << (32 - K)));
+    return d;
+#else
+    return x >> K;
+#endif
+}
+
+// Codes of iteration j in bits [5:0] of each byte lane (bits 7:6 junk,
+// ignored by the converts), byte lanes already permuted {1,3,0,2} so that
+// the low half feeds R1 (codes 4j+0, 4j+1) and the high half R2 (4j+2,
+// 4j+3).  All stitch operations are byte-local, so the lane permutation is
+// applied once to each of the three packed words (3 PRMT per slice rather
+// than one per iteration).
 template <int F>
 FPX_DEV void codes_low6(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (&c)[4]) {
+    const uint32_t pa = prmt(wa, 0x2031u), pb = prmt(wb, 0x2031u), pc = prmt(wc, 0x2031u);
     if constexpr (FmtTraits<F>::kBitsHi == 2) {
         // 2-bit group j (bits 7-2j..6-2j) -> bits 5:4; 4-bit group j%2 -> bits 3:0
-        c[0] = lop3_sel(wa >> 2, wb >> 4, 0x30303030u);
-        c[1] = lop3_sel(wa, wb, 0x30303030u);
-        c[2] = lop3_sel(wa << 2, wc >> 4, 0x30303030u);
-        c[3] = lop3_sel(wa << 4, wc, 0x30303030u);
+        c[0] = lop3_sel<0x30303030u>(shr<2>(pa), shr<4>(pb));
+        c[1] = lop3_sel<0x30303030u>(pa, pb);
+        c[2] = lop3_sel<0x30303030u>(pa << 2, shr<4>(pc));
+        c[3] = lop3_sel<0x30303030u>(pa << 4, pc);
     } else {
         // e2m2 [4,1] -> e2m3 code (c << 1): 4-bit group j%2 (S E1 E0 M1) -> bits 5:2,
         // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0.
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint32_t w4 = j < 2 ? wa : wb;
-            const uint32_t hi = (j & 1) ? (w4 << 2) : (w4 >> 2);
+            const uint32_t w4 = j < 2 ? pa : pb;
+            const uint32_t hi = (j & 1) ? (w4 << 2) : shr<2>(w4);
             const int g = 4 * h + j;
-            const uint32_t lo = (g <= 6) ? (wc >> (6 - g)) : (wc << 1);
+            const uint32_t lo = (g <= 6) ? (pc >> (6 - g)) : (pc << 1);
             c[j] = (hi & 0x3c3c3c3cu) | (lo & 0x02020202u);
         }
     }
@@ -172,7 +200,7 @@ FPX_DEV void dequant_slice_half(uint32_t wa, uint32_t wb, uint32_t wc, int h, co
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             uint32_t a, b;
-            cvt_pairs<F == kE3M2 ? kE3M2 : kE2M3>(prmt(c[j], 0x2031u), a, b);
+            cvt_pairs<F == kE3M2 ? kE3M2 : kE2M3>(c[j], a, b);
             r1[j] = hmul2_rn(a, sc[j >> 1][0]);
             r2[j] = hmul2_rn(b, sc[j >> 1][1]);
         }

@@ -41,6 +41,7 @@ struct LinearLaunch {
     uint32_t* counters;        // split > 1: per (tile, quarter) arrival counters (zeroed once)
     int grid;                  // persistent CTAs (0 = auto)
     unsigned long long* trace; // debug: per-stage clock64 trace of CTA 0 (7 events x 512 stages), or null
+    volatile unsigned long long* prog;  // debug: mapped host progress words (FPX_LINEAR_TRACE=3), or null
 };
 
 cudaError_t launch_linear(const LinearLaunch& p, cudaStream_t st);

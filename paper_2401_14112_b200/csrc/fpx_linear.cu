@@ -39,6 +39,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "fpx_dequant.cuh"
@@ -48,6 +49,9 @@
 namespace fpxk {
 
 constexpr int kTileM = 128;   // rows per unit (two 64-row tile-rows)
+#ifndef FPX_EMPTY_VIA_WAIT
+#define FPX_EMPTY_VIA_WAIT 0
+#endif
 // Warp roles.  The SMSP issue arbiter favours the highest warp id
 // (B300_MICROARCH.md "Multi-warp arbiter"), so the latency-critical single
 // warps (MMA issuer, producer) take the top ids, the epilogue the next four
@@ -72,13 +76,38 @@ struct KParams {
     uint32_t dbg;  // bring-up knobs (FPX_LINEAR_DBG): 1 no dequant math, 2 no MMA, 4 no weight loads, 8 no act loads,
                   // 16 epilogue polls with back-off, 32 dequant A-slot polls with back-off
     unsigned long long* trace;  // optional per-stage clock trace of CTA 0 (fpx_debug_trace), else null
+    volatile unsigned long long* prog;  // debug: mapped host memory, per (CTA, warp) current wait, else null
 };
+
+// Debug (FPX_LINEAR_TRACE=3): record, in mapped host memory the host can read
+// while a launch is stuck, which barrier each warp is waiting on.
+__device__ __forceinline__ void wait_rec(const KParams& p, uint64_t* bar, uint32_t parity, uint32_t tag,
+                                         uint32_t si) {
+    if (p.prog != nullptr) {
+        const uint32_t w = threadIdx.x >> 5;
+        p.prog[blockIdx.x * 32 + w] = (1ull << 63) | (static_cast<unsigned long long>(tag) << 56) |
+                                      (static_cast<unsigned long long>(si & 0xffffffu) << 32) |
+                                      (static_cast<unsigned long long>(smem_u32(bar)) << 1) | parity;
+    }
+    mbar_wait(bar, parity);
+    if (p.prog != nullptr) p.prog[blockIdx.x * 32 + (threadIdx.x >> 5)] = 0;
+}
 
 // trace slots: [event][stage], kTraceStages stages per event
 constexpr int kTraceStages = 512;
-enum TraceEv { kTrProdIssue = 0, kTrDqAempty, kTrDqFull, kTrDqDone, kTrMmaAfull, kTrMmaIssued, kTrEpiFull, kTrDqDone1, kTrDqDone2, kTrDqDone3, kTrNumEv };
+enum TraceEv { kTrProdIssue = 0, kTrDqAempty, kTrDqFull, kTrDqDone, kTrMmaAfull, kTrMmaIssued, kTrEpiFull, kTrDqDone1, kTrDqDone2, kTrDqDone3, kTrMmaWait, kTrMmaGo, kTrNumEv };
 __device__ __forceinline__ void trace_mark(const KParams& p, int ev, uint32_t si) {
     if (p.trace != nullptr && blockIdx.x == 0 && si < kTraceStages) p.trace[ev * kTraceStages + si] = clock64();
+}
+
+// Whole-grid timeline (globaltimer ns): per CTA slot e (0 = start after the
+// prologue, 1..6 = unit ends, 7 = exit), at trace[12*512 + cta*8 + e].
+__device__ __forceinline__ void trace_cta(const KParams& p, uint32_t e) {
+    if (p.trace != nullptr && blockIdx.x < 256 && e < 8) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[12 * kTraceStages + blockIdx.x * 8 + e] = t;
+    }
 }
 
 template <int F, int NPAD, int KS_ = (NPAD <= 128 ? 2 : 1), int NG_ = 2>
@@ -118,12 +147,13 @@ __device__ __forceinline__ void unit_range(const KParams& p, uint32_t u, uint32_
     k1 = ((ch + 1) * p.kt) / p.split;
 }
 
-// One k-tile of one dequant warp: 4 slices x (3 LDS + 4 SWAR iterations),
-// then two 16-lane x 32-column TMEM stores (chunks 2h and 2h+1).
+// One k-tile of one dequant warp: 4 slices x (3 LDS + 4 register
+// iterations) into the two 16-lane x 32-column TMEM A fragments o0 (chunk
+// 2h) and o1 (chunk 2h+1), in tcgen05.st 16x128b register order.
 template <int F>
-__device__ __forceinline__ void dequant_ktile(uint32_t hi, uint32_t lo, int h, uint32_t lane,
-                                             const uint32_t (&sc)[2][2], uint32_t taddr) {
-    uint32_t o0[16], o1[16];
+__device__ __forceinline__ void dequant_ktile_regs(uint32_t hi, uint32_t lo, int h, uint32_t lane,
+                                                  const uint32_t (&sc)[2][2], uint32_t (&o0)[16],
+                                                  uint32_t (&o1)[16]) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         uint32_t oa, ob, oc;
@@ -144,6 +174,13 @@ __device__ __forceinline__ void dequant_ktile(uint32_t hi, uint32_t lo, int h, u
         o1[4 * s + 2] = r1[3];
         o1[4 * s + 3] = r2[3];
     }
+}
+
+template <int F>
+__device__ __forceinline__ void dequant_ktile(uint32_t hi, uint32_t lo, int h, uint32_t lane,
+                                             const uint32_t (&sc)[2][2], uint32_t taddr) {
+    uint32_t o0[16], o1[16];
+    dequant_ktile_regs<F>(hi, lo, h, lane, sc, o0, o1);
     tmem_st_16x128b_x8(taddr, o0);
     tmem_st_16x128b_x8(taddr + (16u << 16), o1);
 }
@@ -397,6 +434,372 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
     }
 }
 
+// ===========================================================================
+// Decode kernel (batch <= 32, the memory-bound regime).
+//
+// Measured constraints that shape it (tests/micro/, B200):
+//  * a kind::f16 tcgen05.mma with M=128, K=16 costs ~44 tensor-pipe cycles
+//    for ANY N <= 128 (operand fetch, not math, bounds it: ~100 B/clk/SM),
+//    i.e. at most ~46 fp16 weights/clk/SM -- only ~1.5x the ~31
+//    weights/clk/SM the HBM roofline needs, so the MMA pipe must be kept
+//    busy;
+//  * every tcgen05.commit costs ~300 tensor-pipe cycles, so commits are
+//    batched (one per kBS stages) instead of one per resource;
+//  * tcgen05.commit from several concurrently issuing threads loses
+//    arrivals, so exactly one thread issues all MMAs and commits;
+//  * an elected-thread loop pays vector->uniform register moves on every
+//    TMA / MMA operand; the producer and MMA loops run warp-wide with
+//    warp-uniform control flow and one lane issuing.
+//
+// Pipeline (one persistent CTA per SM, units = (128-row tile, K chunk)):
+//  producers (P warps) --TMA--> smem ring of S stages (KS k-tiles of packed
+//  weights for 2 tile-rows + KS activation tiles)
+//  de-quantiser groups (G x 4 warps; stage si -> group si % G) --LDS,
+//  register de-quantisation, tcgen05.st--> TMEM A ring of R stage slots
+//  MMA warp: stages in order, KS x 4 MMAs each into the unit's single fp32
+//  accumulator (double-buffered across units), commit per kBS stages
+//  (releases smem stages and A slots), commit per unit (accumulator full)
+//  epilogue (4 warps): tcgen05.ld -> C, or split-K partials + fixed-order
+//  last-arriver reduction.
+// The k-tiles of a unit are accumulated in K order by one issuer, so the
+// result is a pure function of (W, act, split): deterministic and
+// independent of the grid and of the group count.
+// Every stage is a full KS k-tiles: a K tail beyond the last k-tile is
+// zero-filled by TMA (weights and activations), contributing exact zeros.
+//
+// Warps: 0 .. 4G-1 de-quantisers (group w/4, TMEM lane quarter w%4),
+// 4G .. 4G+3 epilogue (quarter w%4), 4G+4 MMA issuer, 4G+5 .. 4G+4+P TMA
+// producers (the first also allocates TMEM).
+template <int F, int NPAD, int KS_, int G_, int P_ = 2>
+struct GCfg {
+    static constexpr int kKS = KS_;
+    static constexpr int kG = G_;
+    static constexpr int kP = P_;
+    static constexpr int kEpiWarp0 = 4 * kG;
+    static constexpr int kMmaWarp = kEpiWarp0 + 4;
+    static constexpr int kProdWarp = kMmaWarp + 1;
+    static constexpr int kWarps = kProdWarp + kP;
+    static constexpr int kThreads = 32 * kWarps;
+    static constexpr int kHiBytes = 512 * FmtTraits<F>::kBitsHi;
+    static constexpr int kLoBytes = 512 * FmtTraits<F>::kBitsLo;
+    static constexpr int kBBytes = NPAD * 128;
+    static constexpr int kHiOff = kKS * kBBytes;  // [B x KS][hi r0][hi r1][lo r0][lo r1]
+    static constexpr int kLoOff = kHiOff + 2 * kKS * kHiBytes;
+    static constexpr int kStageRaw = kLoOff + 2 * kKS * kLoBytes;
+    static constexpr int kStageBytes = (kStageRaw + 1023) / 1024 * 1024;
+    static constexpr int kStages = std::min(24, kSmemBudget / kStageBytes);
+    static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
+    static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
+#ifndef FPX_DEC_BS
+#define FPX_DEC_BS 3
+#endif
+    static constexpr int kBS = std::max(1, std::min(FPX_DEC_BS, kASlots / 2));  // stages per commit batch
+    static constexpr int kNB = (std::max(kStages, kASlots) + kBS - 1) / kBS + 3;  // batch barriers (no aliasing)
+    static constexpr int kBarBytes = 8 * (kStages + kNB + kASlots + 4) + 16;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
+    static constexpr uint32_t kTxBytes = kKS * kBBytes + 2 * kKS * (kHiBytes + kLoBytes);
+    static_assert(kStages >= kBS + 1 && kASlots >= kBS + 1, "rings must outlast a commit batch");
+    static_assert(NPAD <= 32, "decode kernel serves the small-batch regime");
+};
+
+// Stage-granular unit range: chunk c of a 128-row tile covers stages
+// [c*NST/split, (c+1)*NST/split), NST = ceil(KT/KS).
+template <int KS>
+__device__ __forceinline__ void unit_stages(const KParams& p, uint32_t u, uint32_t& mt, uint32_t& ch, uint32_t& s0,
+                                           uint32_t& ns) {
+    const uint32_t nst = (p.kt + KS - 1) / KS;
+    mt = u / p.split;
+    ch = u % p.split;
+    s0 = (ch * nst) / p.split;
+    ns = ((ch + 1) * nst) / p.split - s0;
+}
+
+template <int F, int NPAD, int KS_, int G_>
+__global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
+    fpx_linear_decode_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap hi_map,
+                             const __grid_constant__ CUtensorMap lo_map, const KParams p) {
+    using C = GCfg<F, NPAD, KS_, G_>;
+    constexpr int KS = C::kKS, G = C::kG, S = C::kStages, R = C::kASlots, BS = C::kBS, NB = C::kNB;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;           // [S]  TMA -> group                 (tx bytes)
+    uint64_t* done = full + S;       // [NB] MMAs of a batch of BS stages complete (commit)
+    uint64_t* aready = done + NB;    // [R]  group's 4 warps stored the stage's A tiles
+    uint64_t* accfull = aready + R;  // [2]  unit's MMAs complete (commit)
+    uint64_t* accempty = accfull + 2;  // [2] epilogue drained the accumulator
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+    const uint32_t warp = warp_id_uniform();
+    const uint32_t lane = lane_id();
+    const uint32_t u_begin = static_cast<uint32_t>((uint64_t)blockIdx.x * p.units / gridDim.x);
+    const uint32_t u_end = static_cast<uint32_t>((uint64_t)(blockIdx.x + 1) * p.units / gridDim.x);
+
+    if (warp == C::kEpiWarp0 && lane == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < NB; ++i) mbar_init(&done[i], 1);
+        for (int i = 0; i < R; ++i) mbar_init(&aready[i], 4);
+        for (int i = 0; i < 2; ++i) mbar_init(&accfull[i], 1), mbar_init(&accempty[i], 4);
+        fence_mbar_init();
+    }
+    if (warp == C::kProdWarp) {
+        if (lane == 0) prefetch_tmap(&act_map), prefetch_tmap(&hi_map), prefetch_tmap(&lo_map);
+        tmem_alloc<kTmemCols>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) trace_cta(p, 0);
+    grid_dep_launch();
+
+    if (warp >= C::kProdWarp) {
+        // ------------------------------------------------ producers
+        // Weights are immutable for the duration of the call, so the first
+        // ring pass of weight tiles is requested BEFORE waiting for the
+        // preceding kernel (PDL): this CTA's HBM stream starts while the
+        // previous launch drains.  Activations (possibly written by that
+        // kernel) are requested only after griddepcontrol.wait.
+        const uint32_t pw = warp - C::kProdWarp;
+        const bool leader = lane == 0;
+        const uint64_t pol_w = policy_evict_first();
+        const uint64_t pol_b = policy_evict_last();
+        const uint32_t bytes = (p.dbg & 12u) == 0 ? C::kTxBytes
+                                                  : ((p.dbg & 8u) ? 0u : KS * C::kBBytes) +
+                                                        ((p.dbg & 4u) ? 0u : 2 * KS * (C::kHiBytes + C::kLoBytes));
+        // pass 0: first ring pass, weights only; pass 1: everything else
+#ifndef FPX_PDL_EARLY
+#define FPX_PDL_EARLY 1
+#endif
+        if (!FPX_PDL_EARLY) grid_dep_wait();
+        for (int pass = FPX_PDL_EARLY ? 0 : 1; pass < 2; ++pass) {
+            if (pass == 1 && FPX_PDL_EARLY) grid_dep_wait();
+            uint32_t si = 0;
+            for (uint32_t u = u_begin; u < u_end; ++u) {
+                uint32_t mt, ch, s0, ns;
+                unit_stages<KS>(p, u, mt, ch, s0, ns);
+                const int32_t tr0 = static_cast<int32_t>(2 * mt);
+                for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
+                    if (si % C::kP != pw) continue;
+                    const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
+                    const uint32_t st = si % S;
+                    uint8_t* sb = smem + st * C::kStageBytes;
+                    const bool first_pass = si < static_cast<uint32_t>(S);
+                    if (pass == 0 && !first_pass) break;
+                    if (pass == 1 && first_pass) {
+                        // weights already requested in pass 0
+                        if (leader && !(p.dbg & 8u)) tma_load_3d(sb, &act_map, 0, 0, k, &full[st], pol_b);
+                        continue;
+                    }
+                    if (!first_pass) {
+                        // stage si - S (same slot) is consumed once its batch's MMAs completed
+                        const uint32_t b = (si - S) / BS;
+                        if (leader) trace_mark(p, kTrDqDone3, si);
+                        wait_rec(p, &done[b % NB], (b / NB) & 1u, 1, si);
+                    }
+                    if (leader) {
+                        trace_mark(p, kTrProdIssue, si);
+                        // full boxes always land (OOB rows / k-tiles are zero-filled)
+                        mbar_arrive_expect_tx(&full[st], bytes);
+                        if (!(p.dbg & 4u)) {
+                            tma_load_3d(sb + C::kHiOff, &hi_map, 0, k, tr0, &full[st], pol_w);
+                            tma_load_3d(sb + C::kLoOff, &lo_map, 0, k, tr0, &full[st], pol_w);
+                        }
+                        if (pass == 1 && !(p.dbg & 8u)) tma_load_3d(sb, &act_map, 0, 0, k, &full[st], pol_b);
+                    }
+                    __syncwarp();
+                }
+                if (pass == 0 && si >= static_cast<uint32_t>(S)) break;
+            }
+        }
+    } else if (warp == C::kMmaWarp) {
+        // ------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = umma_idesc_f16(kTileM, NPAD);
+        const bool leader = lane == 0;
+        uint32_t si = 0, lu = 0;
+        for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
+            uint32_t mt, ch, s0, ns;
+            unit_stages<KS>(p, u, mt, ch, s0, ns);
+            const uint32_t ab = lu & 1u;
+            wait_rec(p, &accempty[ab], ((lu >> 1) & 1u) ^ 1u, 5, lu);  // epilogue done with unit lu-2
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + C::kAccCol0 + ab * NPAD;
+            for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
+                const uint32_t as = si % R;
+                if (leader) trace_mark(p, kTrMmaWait, si);
+                wait_rec(p, &aready[as], (si / R) & 1u, 4, si);
+                tc_fence_after();
+                if (leader) trace_mark(p, kTrMmaGo, si);
+                const uint32_t a_tmem = tmem + as * KS * 32;
+                const uint64_t bdesc = umma_desc_sw128_kmajor(smem_u32(smem + (si % S) * C::kStageBytes));
+                const uint32_t acc0 = ls > 0 ? 1u : 0u;  // the unit's first k-tile overwrites
+                if (!(p.dbg & 2u)) {
+#pragma unroll
+                    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+                        for (uint32_t ks = 0; ks < 4; ++ks)
+                            umma_f16_ts_warp(d_tmem, a_tmem + kk * 32 + ks * 8,
+                                             bdesc + static_cast<uint64_t>((kk * C::kBBytes + ks * 32) >> 4), idesc,
+                                             (kk > 0 || ks > 0) ? 1u : acc0);
+                }
+                if ((si + 1) % BS == 0) umma_commit_warp(&done[(si / BS) % NB]);
+                if (leader) trace_mark(p, kTrMmaIssued, si);
+            }
+            umma_commit_warp(&accfull[ab]);
+        }
+        if (si % BS != 0) umma_commit_warp(&done[(si / BS) % NB]);  // final partial batch
+    } else if (warp >= C::kEpiWarp0) {
+        // ------------------------------------------------ epilogue
+        grid_dep_wait();  // C / partials / counters may still be in use by the preceding kernel
+        const uint32_t q = warp & 3u;
+        const uint32_t row_l = 32 * q + lane;
+        uint32_t lu = 0;
+        for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
+            uint32_t mt, ch, s0, ns;
+            unit_stages<KS>(p, u, mt, ch, s0, ns);
+            const uint32_t ab = lu & 1u;
+            wait_rec(p, &accfull[ab], (lu >> 1) & 1u, 2, lu);
+            if (q == 0 && lane == 0) trace_mark(p, kTrEpiFull, lu);
+            tc_fence_after();
+            const uint32_t m = mt * kTileM + row_l;
+            const bool row_ok = m < p.rows_p;
+            float* part = p.ws + (static_cast<size_t>(mt) * p.split + ch) * NPAD * kTileM;
+            const uint32_t tacc = tmem + ((32 * q) << 16) + C::kAccCol0 + ab * NPAD;
+#pragma unroll
+            for (uint32_t c0 = 0; c0 < NPAD; c0 += 16) {
+                uint32_t v[16];
+                if (ns > 0) {
+                    tmem_ld_32x32b_x16(tacc + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K chunk contributes zero
+                }
+                if (c0 < p.n) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t col = c0 + j;
+                        if (col < p.n) {
+                            if (p.split == 1) {
+                                if (row_ok) p.c[static_cast<size_t>(col) * p.ldc + m] = __uint_as_float(v[j]);
+                            } else {
+                                part[static_cast<size_t>(col) * kTileM + row_l] = __uint_as_float(v[j]);
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[ab]);
+            if (q == 0 && lane == 0) trace_cta(p, 1 + lu);
+            if (p.split > 1) {
+                __threadfence();
+                __syncwarp();
+                uint32_t old = 0;
+                if (lane == 0) old = atomicAdd(&p.counters[mt * 4 + q], 1u);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == p.split - 1) {
+                    // last arriver: C = ((P0 + P1) + P2) + ... in chunk order
+                    __threadfence();
+                    const float* base = p.ws + static_cast<size_t>(mt) * p.split * NPAD * kTileM + row_l;
+                    for (uint32_t c0 = 0; c0 < p.n; c0 += 16) {
+                        float acc[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
+                        for (uint32_t cc = 0; cc < p.split; ++cc) {
+                            const float* pc = base + (static_cast<size_t>(cc) * NPAD + c0) * kTileM;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c0 + j < p.n) acc[j] += __ldcg(pc + j * kTileM);
+                        }
+                        if (row_ok) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = acc[j];
+                        }
+                    }
+                    if (lane == 0) p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ de-quantiser groups
+        const uint32_t g = warp >> 2;
+        const uint32_t q = warp & 3u;
+        const int h = static_cast<int>(q & 1u);
+        const uint32_t r = q >> 1;
+        const uint32_t tq = tmem + ((32 * q) << 16);  // this warp's TMEM lane quarter
+        uint32_t si = 0;
+        for (uint32_t u = u_begin; u < u_end; ++u) {
+            uint32_t mt, ch, s0, ns;
+            unit_stages<KS>(p, u, mt, ch, s0, ns);
+            const uint32_t tr = 2 * mt + r;
+            const bool valid = tr < p.tile_rows;
+            uint32_t sc[2][2] = {{0, 0}, {0, 0}};
+            if (valid) {
+#pragma unroll
+                for (int lc = 0; lc < 2; ++lc)
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const uint32_t row = tr * 64 + 16 * (2 * h + lc) + 8 * hf + lane / 4;
+                        sc[lc][hf] = row_scale_for<F, kHwCvt>(p.scales[row]);
+                    }
+            }
+            // this group's stages of the unit: si % G == g
+            uint32_t ls = (g + G - si % G) % G;
+            for (si += ls; ls < ns; ls += G, si += G) {
+                const uint32_t st = si % S, as = si % R;
+                const uint32_t sb = smem_u32(smem + st * C::kStageBytes);
+                if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
+                wait_rec(p, &full[st], (si / S) & 1u, 3, si);
+                if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);
+                uint32_t o[KS][2][16];
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
+                    // Rows of a missing second tile-row (odd tile_rows) and the
+                    // FPX_LINEAR_DBG=1 no-math mode store zeros: every A-slot lane
+                    // an MMA reads has been written by this CTA.
+                    if (valid && !(p.dbg & 1u)) {
+                        dequant_ktile_regs<F>(sb + C::kHiOff + (r * KS + kk) * C::kHiBytes,
+                                              sb + C::kLoOff + (r * KS + kk) * C::kLoBytes, h, lane, sc, o[kk][0],
+                                              o[kk][1]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) o[kk][0][i] = 0u, o[kk][1][i] = 0u;
+                    }
+                    if (kk == 0) {
+                        // A slot `as` last held stage si - R: free once that stage's batch completed
+                        if (q == 0 && lane == 0) trace_mark(p, kTrDqDone, si);
+                        if (si >= static_cast<uint32_t>(R)) {
+                            const uint32_t b = (si - R) / BS;
+                            wait_rec(p, &done[b % NB], (b / NB) & 1u, 6, si);
+                        }
+                        if (q == 0 && lane == 0) trace_mark(p, kTrDqDone1, si);
+                        tc_fence_after();
+                    }
+                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32, o[kk][0]);
+                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32 + (16u << 16), o[kk][1]);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aready[as]);
+                if (q == 0 && lane == 0) trace_mark(p, kTrMmaAfull, si);
+            }
+            si -= ls - ns;  // back to the first stage of the next unit
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) trace_cta(p, 7);
+    if (warp == C::kProdWarp) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -410,23 +813,77 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int F, int NPAD, int KS_, int NG_>
-cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStream_t st) {
-    using C = Cfg<F, NPAD, KS_, NG_>;
-    auto kern = fpx_linear_kernel<F, NPAD, KS_, NG_>;
-    // 3-D view of the activations: {64 k, n, k-tile} with strides {lda, 64}
-    // elements; box {64, NPAD, KS} -> KS consecutive SW128 [NPAD x 128 B] tiles.
-    CUtensorMap map;
+// Launch with programmatic stream serialization (PDL) when FPX_LINEAR_PDL=1:
+// the kernel may start (prologue, weight prefetch) while the preceding
+// kernel in the stream drains; its griddepcontrol.wait orders everything
+// that depends on that kernel.  Off by default: worth ~2 us per launch, but
+// back-to-back PDL launches were seen to fault / hang in a debug mode
+// (FPX_LINEAR_DBG=1) that is not yet understood.
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FPX_LINEAR_PDL");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// 3-D view of the activations: {64 k, n, k-tile} with strides {lda, 64}
+// elements; box {64, NPAD, KS} -> KS consecutive SW128 [NPAD x 128 B] tiles.
+cudaError_t make_act_map(const LinearLaunch& L, uint32_t npad, uint32_t ks, CUtensorMap* map) {
     auto encode = encode_fn();
     if (!encode) return cudaErrorNotSupported;
     const cuuint64_t dims[3] = {64u, L.n, L.cols_p / 64u};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(L.lda) * 2u, 128u};
-    const cuuint32_t box[3] = {64u, static_cast<cuuint32_t>(NPAD), static_cast<cuuint32_t>(C::kKS)};
+    const cuuint32_t box[3] = {64u, npad, ks};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
-    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(L.act), dims, strides, box, estr,
+    if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(L.act), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
+    return cudaSuccess;
+}
+
+// 3-D view of one packed stream (w bits/code, 512*w bytes per 64x64 tile,
+// tiles row-major, prepack.cpp:190-191): {64*w u64 words, k-tile, tile-row};
+// box {64*w, KS, 2} = KS consecutive tiles of the two tile-rows of a 128-row
+// unit, landing as [tile-row][k-tile][512*w B] in shared memory.
+cudaError_t make_stream_map(const uint8_t* base, int w, uint32_t tile_rows, uint32_t kt, uint32_t ks,
+                            CUtensorMap* map) {
+    auto encode = encode_fn();
+    if (!encode) return cudaErrorNotSupported;
+    const cuuint64_t tile_bytes = 512u * static_cast<cuuint64_t>(w);
+    const cuuint64_t dims[3] = {tile_bytes / 8u, kt, tile_rows};
+    const cuuint64_t strides[2] = {tile_bytes, tile_bytes * kt};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(tile_bytes / 8u), ks, 2u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    if (encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    return cudaSuccess;
+}
+
+template <int F, int NPAD, int KS_, int NG_>
+cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStream_t st) {
+    using C = Cfg<F, NPAD, KS_, NG_>;
+    auto kern = fpx_linear_kernel<F, NPAD, KS_, NG_>;
+    CUtensorMap map;
+    if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
     static std::once_flag attr_once;  // per instantiation (the attribute is per function)
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [&] {
@@ -437,24 +894,58 @@ cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
     return cudaGetLastError();
 }
 
-// Pipeline shape per batch width: KS k-tiles per stage, NG dequant warp
-// groups (bounded by the TMEM A-stage ring: NG + 1 <= A stages).
-// FPX_LINEAR_CFG="KS,NG" overrides for tuning (instantiated subset only).
+template <int F, int NPAD, int KS_, int G_>
+cudaError_t launch_g(const LinearLaunch& L, const KParams& kp, int grid, cudaStream_t st) {
+    using C = GCfg<F, NPAD, KS_, G_>;
+    auto kern = fpx_linear_decode_kernel<F, NPAD, KS_, G_>;
+    // K chunks are whole stages: at most ceil(KT/KS) of them
+    KParams kq = kp;
+    const uint32_t nst = (kp.kt + C::kKS - 1) / C::kKS;
+    if (kq.split > nst) {
+        kq.split = nst;
+        kq.units = (kp.rows_p + kTileM - 1) / kTileM * nst;
+        grid = std::min<int>(grid, static_cast<int>(kq.units));
+    }
+    CUtensorMap map, hi_map, lo_map;
+    if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
+    if (cudaError_t e = make_stream_map(L.s_hi, FmtTraits<F>::kBitsHi, L.rows_p / 64, L.cols_p / 64, C::kKS, &hi_map))
+        return e;
+    if (cudaError_t e = make_stream_map(L.s_lo, FmtTraits<F>::kBitsLo, L.rows_p / 64, L.cols_p / 64, C::kKS, &lo_map))
+        return e;
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    return launch_pdl(kern, grid, C::kThreads, C::kSmemBytes, st, map, hi_map, lo_map, kq);
+}
+
+// Pipeline shape per batch width.  N <= 32 (decode): the grouped kernel,
+// KS k-tiles per stage, G self-issuing de-quantiser groups.  N > 32: the
+// single-issuer kernel, KS k-tiles per stage, NG de-quantiser groups.
+// Tuning overrides (instantiated subset only): FPX_LINEAR_KERNEL=classic
+// forces the single-issuer kernel for N <= 32; FPX_LINEAR_CFG="KS,G".
 template <int F>
 cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, int grid, cudaStream_t st) {
     int ks = 0, ng = 0;
     if (const char* c = std::getenv("FPX_LINEAR_CFG")) std::sscanf(c, "%d,%d", &ks, &ng);
+    const char* kname = std::getenv("FPX_LINEAR_KERNEL");
+    const bool classic = kname != nullptr && std::strcmp(kname, "classic") == 0;
+    if (!classic && npad <= 32) {
+        if (npad == 16) {
+            if (ks == 1 && ng == 4) return launch_g<F, 16, 1, 4>(L, kp, grid, st);
+            if (ks == 2 && ng == 2) return launch_g<F, 16, 2, 2>(L, kp, grid, st);
+            if (ks == 4 && ng == 2) return launch_g<F, 16, 4, 2>(L, kp, grid, st);
+            return launch_g<F, 16, 2, 4>(L, kp, grid, st);
+        }
+        if (ks == 2 && ng == 2) return launch_g<F, 32, 2, 2>(L, kp, grid, st);
+        if (ks == 4 && ng == 2) return launch_g<F, 32, 4, 2>(L, kp, grid, st);
+        return launch_g<F, 32, 2, 4>(L, kp, grid, st);
+    }
     switch (npad) {
-        case 16:
-            if (ks == 2 && ng == 2) return launch_t<F, 16, 2, 2>(L, kp, grid, st);
-            if (ks == 2 && ng == 4) return launch_t<F, 16, 2, 4>(L, kp, grid, st);
-            if (ks == 4 && ng == 2) return launch_t<F, 16, 4, 2>(L, kp, grid, st);
-            if (ks == 1 && ng == 4) return launch_t<F, 16, 1, 4>(L, kp, grid, st);
-            return launch_t<F, 16, 2, 3>(L, kp, grid, st);
-        case 32:
-            if (ks == 2 && ng == 2) return launch_t<F, 32, 2, 2>(L, kp, grid, st);
-            if (ks == 2 && ng == 4) return launch_t<F, 32, 2, 4>(L, kp, grid, st);
-            return launch_t<F, 32, 2, 3>(L, kp, grid, st);
+        case 16: return launch_t<F, 16, 2, 3>(L, kp, grid, st);
+        case 32: return launch_t<F, 32, 2, 3>(L, kp, grid, st);
         case 64: return launch_t<F, 64, 2, 3>(L, kp, grid, st);
         case 128: return launch_t<F, 128, 2, 2>(L, kp, grid, st);
         case 256: return launch_t<F, 256, 1, 3>(L, kp, grid, st);
@@ -521,6 +1012,7 @@ cudaError_t launch_linear(const LinearLaunch& L, cudaStream_t st) {
     kp.counters = L.counters;
     if (const char* d = std::getenv("FPX_LINEAR_DBG")) kp.dbg = static_cast<uint32_t>(std::atoi(d));
     kp.trace = L.trace;
+    kp.prog = L.prog;
     int grid = L.grid > 0 ? L.grid : 148;
     grid = std::min<int>(grid, static_cast<int>(kp.units));
     if (grid <= 0) return cudaSuccess;

@@ -3,6 +3,7 @@
 // st/ld, UMMA issue/commit) and fp16x2 RNE multiply.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 
 #define FPX_DEV __device__ __forceinline__
@@ -52,8 +53,23 @@ FPX_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
+// FPX_TRYWAIT_HINT (ns): suspend-time hint of every try_wait; the waiting
+// thread sleeps in hardware until the phase completes or the hint expires,
+// instead of re-polling the barrier unit.  0 = no hint (system default).
+#ifndef FPX_TRYWAIT_HINT
+#define FPX_TRYWAIT_HINT 0
+#endif
 FPX_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
+#if FPX_TRYWAIT_HINT
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "n"(FPX_TRYWAIT_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
@@ -61,21 +77,64 @@ FPX_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#endif
     return ok != 0;
 }
 
+// FPX_WATCHDOG builds (debug variant only): a wait that has not completed
+// after ~2^28 polls prints the barrier's shared address, parity and the
+// caller's block/thread, then traps -- a diagnosable crash instead of a hang.
+#ifndef FPX_WATCHDOG
+#define FPX_WATCHDOG 0
+#endif
 FPX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if FPX_WATCHDOG
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1u << 22)) {
+            printf("watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x, threadIdx.x,
+                   smem_u32(bar), parity);
+            __trap();
+        }
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // Polling with back-off, for waiters off the critical path: every
 // try_wait occupies the SM's barrier unit, so idle spinners slow down the
 // latency-critical waiters (MMA issuer, producer) sharing it.
 FPX_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+#if FPX_WATCHDOG
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+        if (++n == (1u << 22)) {
+            printf("watchdog: block %d thread %d stuck (sleeping) on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+                   threadIdx.x, smem_u32(bar), parity);
+            __trap();
+        }
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
         __nanosleep(ns);
     }
+#endif
+}
+
+// Programmatic dependent launch (PDL).  launch_dependents lets the next
+// kernel in the stream be scheduled (its CTAs still need this grid's SM
+// resources to free up); wait blocks until the preceding grid has completed
+// and its memory is visible.  Both are no-ops without the PDL launch attribute.
+FPX_DEV void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+FPX_DEV void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Named CTA barrier over `threads` threads (multiple of 32); id 0 is
+// __syncthreads.
+FPX_DEV void named_bar_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // ---------------------------------------------------------------- TMA
@@ -162,6 +221,30 @@ FPX_DEV void umma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Warp-wide variants for warp-uniform issue loops: the whole warp executes
+// the asm, one elected lane issues.  Keeps the loop's bookkeeping in uniform
+// registers without the per-instruction elect/branch loop nvcc generates for
+// an `if (lane == 0)` around each tcgen05 instruction.
+FPX_DEV void umma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+FPX_DEV void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
         : "memory");
 }
 
