@@ -176,6 +176,41 @@ __device__ __forceinline__ void dequant_ktile_regs(uint32_t hi, uint32_t lo, int
     }
 }
 
+// The same k-tile split into its shared-memory reads (12 words) and the
+// register-only de-quantisation, so a stage's shared memory can be released
+// before the math runs.
+template <int F>
+__device__ __forceinline__ void load_ktile_words(uint32_t hi, uint32_t lo, int h, uint32_t lane,
+                                                 uint32_t (&w)[12]) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        uint32_t oa, ob, oc;
+        bool ah, bh, chh;
+        slice_word_offsets<F>(s, h, lane, oa, ob, oc, ah, bh, chh);
+        w[3 * s + 0] = lds32((ah ? hi : lo) + oa);
+        w[3 * s + 1] = lds32((bh ? hi : lo) + ob);
+        w[3 * s + 2] = lds32((chh ? hi : lo) + oc);
+    }
+}
+
+template <int F>
+__device__ __forceinline__ void dequant_words(const uint32_t (&w)[12], int h, const uint32_t (&sc)[2][2],
+                                              uint32_t (&o0)[16], uint32_t (&o1)[16]) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        uint32_t r1[4], r2[4];
+        dequant_slice_half<F, kHwCvt>(w[3 * s], w[3 * s + 1], w[3 * s + 2], h, sc, r1, r2);
+        o0[4 * s + 0] = r1[0];
+        o0[4 * s + 1] = r2[0];
+        o0[4 * s + 2] = r1[1];
+        o0[4 * s + 3] = r2[1];
+        o1[4 * s + 0] = r1[2];
+        o1[4 * s + 1] = r2[2];
+        o1[4 * s + 2] = r1[3];
+        o1[4 * s + 3] = r2[3];
+    }
+}
+
 template <int F>
 __device__ __forceinline__ void dequant_ktile(uint32_t hi, uint32_t lo, int h, uint32_t lane,
                                              const uint32_t (&sc)[2][2], uint32_t taddr) {
@@ -438,32 +473,36 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
 // Decode kernel (batch <= 32, the memory-bound regime).
 //
 // Measured constraints that shape it (tests/micro/, B200):
-//  * a kind::f16 tcgen05.mma with M=128, K=16 costs ~44 tensor-pipe cycles
-//    for ANY N <= 128 (operand fetch, not math, bounds it: ~100 B/clk/SM),
-//    i.e. at most ~46 fp16 weights/clk/SM -- only ~1.5x the ~31
-//    weights/clk/SM the HBM roofline needs, so the MMA pipe must be kept
-//    busy;
+//  * a kind::f16 tcgen05.mma with M=128, K=16 occupies the tensor pipe for
+//    ~44 cycles for ANY N <= 128 (operand fetch, not math, bounds it), i.e.
+//    at most ~46 fp16 weights/clk/SM -- only ~1.5x the ~31 weights/clk/SM
+//    the HBM roofline needs;
 //  * every tcgen05.commit costs ~300 tensor-pipe cycles, so commits are
-//    batched (one per kBS stages) instead of one per resource;
+//    batched (one per kBS stages);
 //  * tcgen05.commit from several concurrently issuing threads loses
 //    arrivals, so exactly one thread issues all MMAs and commits;
-//  * an elected-thread loop pays vector->uniform register moves on every
-//    TMA / MMA operand; the producer and MMA loops run warp-wide with
-//    warp-uniform control flow and one lane issuing.
+//  * loops that issue TMA / MMA run warp-wide with warp-uniform control flow
+//    (bookkeeping in uniform registers) and elect one lane per instruction
+//    inside the asm.
 //
 // Pipeline (one persistent CTA per SM, units = (128-row tile, K chunk)):
-//  producers (P warps) --TMA--> smem ring of S stages (KS k-tiles of packed
-//  weights for 2 tile-rows + KS activation tiles)
-//  de-quantiser groups (G x 4 warps; stage si -> group si % G) --LDS,
-//  register de-quantisation, tcgen05.st--> TMEM A ring of R stage slots
+//  producers (P warps) --TMA--> weight ring (SW stages: KS k-tiles of packed
+//    weights for the unit's 2 tile-rows) and activation ring (SB stages: KS
+//    activation k-tiles, the MMA's B operand)
+//  de-quantiser groups (G x 4 warps; stage si -> group si % G): LDS the
+//    stage's packed words, release the weight stage at once (it is consumed
+//    in registers), de-quantise, tcgen05.st into the TMEM A ring (R slots)
 //  MMA warp: stages in order, KS x 4 MMAs each into the unit's single fp32
-//  accumulator (double-buffered across units), commit per kBS stages
-//  (releases smem stages and A slots), commit per unit (accumulator full)
+//    accumulator (double-buffered across units); one commit per kBS stages
+//    releases their activation stages and A slots; one commit per unit
+//    hands the accumulator to the epilogue
 //  epilogue (4 warps): tcgen05.ld -> C, or split-K partials + fixed-order
-//  last-arriver reduction.
-// The k-tiles of a unit are accumulated in K order by one issuer, so the
-// result is a pure function of (W, act, split): deterministic and
-// independent of the grid and of the group count.
+//    last-arriver reduction.
+// The weight ring -- where the bytes are -- recycles as soon as the packed
+// words are in registers; only the small activation and A rings wait for
+// MMA completion.  The k-tiles of a unit are accumulated in K order by one
+// issuer, so the result is a pure function of (W, act, split):
+// deterministic and independent of the grid and of the group count.
 // Every stage is a full KS k-tiles: a K tail beyond the last k-tile is
 // zero-filled by TMA (weights and activations), contributing exact zeros.
 //
@@ -480,25 +519,27 @@ struct GCfg {
     static constexpr int kProdWarp = kMmaWarp + 1;
     static constexpr int kWarps = kProdWarp + kP;
     static constexpr int kThreads = 32 * kWarps;
-    static constexpr int kHiBytes = 512 * FmtTraits<F>::kBitsHi;
+    static constexpr int kHiBytes = 512 * FmtTraits<F>::kBitsHi;  // per 64x64 tile
     static constexpr int kLoBytes = 512 * FmtTraits<F>::kBitsLo;
-    static constexpr int kBBytes = NPAD * 128;
-    static constexpr int kHiOff = kKS * kBBytes;  // [B x KS][hi r0][hi r1][lo r0][lo r1]
-    static constexpr int kLoOff = kHiOff + 2 * kKS * kHiBytes;
-    static constexpr int kStageRaw = kLoOff + 2 * kKS * kLoBytes;
-    static constexpr int kStageBytes = (kStageRaw + 1023) / 1024 * 1024;
-    static constexpr int kStages = std::min(24, kSmemBudget / kStageBytes);
+    static constexpr int kBBytes = NPAD * 128;                    // per activation k-tile
+    // weight stage: [hi r0 x KS][hi r1 x KS][lo r0 x KS][lo r1 x KS]
+    static constexpr int kLoOff = 2 * kKS * kHiBytes;
+    static constexpr int kWStageBytes = (2 * kKS * (kHiBytes + kLoBytes) + 1023) / 1024 * 1024;
+    static constexpr int kBStageBytes = (kKS * kBBytes + 1023) / 1024 * 1024;
+    static constexpr int kBStages = std::min(16, (kSmemBudget / 3) / kBStageBytes);
+    static constexpr int kWStages = std::min(16, (kSmemBudget - kBStages * kBStageBytes) / kWStageBytes);
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
     static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
 #ifndef FPX_DEC_BS
 #define FPX_DEC_BS 3
 #endif
     static constexpr int kBS = std::max(1, std::min(FPX_DEC_BS, kASlots / 2));  // stages per commit batch
-    static constexpr int kNB = (std::max(kStages, kASlots) + kBS - 1) / kBS + 3;  // batch barriers (no aliasing)
-    static constexpr int kBarBytes = 8 * (kStages + kNB + kASlots + 4) + 16;
-    static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
-    static constexpr uint32_t kTxBytes = kKS * kBBytes + 2 * kKS * (kHiBytes + kLoBytes);
-    static_assert(kStages >= kBS + 1 && kASlots >= kBS + 1, "rings must outlast a commit batch");
+    static constexpr int kNB = (std::max(kBStages, kASlots) + kBS - 1) / kBS + 3;  // batch barriers (no aliasing)
+    static constexpr int kBarBytes = 8 * (2 * kWStages + kBStages + kNB + kASlots + 4) + 16;
+    static constexpr int kSmemBytes = kWStages * kWStageBytes + kBStages * kBStageBytes + kBarBytes + 1024;
+    static constexpr uint32_t kWTx = 2 * kKS * (kHiBytes + kLoBytes);
+    static constexpr uint32_t kBTx = kKS * kBBytes;
+    static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
     static_assert(NPAD <= 32, "decode kernel serves the small-batch regime");
 };
 
@@ -519,15 +560,20 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     fpx_linear_decode_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap hi_map,
                              const __grid_constant__ CUtensorMap lo_map, const KParams p) {
     using C = GCfg<F, NPAD, KS_, G_>;
-    constexpr int KS = C::kKS, G = C::kG, S = C::kStages, R = C::kASlots, BS = C::kBS, NB = C::kNB;
+    constexpr int KS = C::kKS, G = C::kG, SW = C::kWStages, SB = C::kBStages, R = C::kASlots, BS = C::kBS,
+                  NB = C::kNB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
-    uint64_t* full = bars;           // [S]  TMA -> group                 (tx bytes)
-    uint64_t* done = full + S;       // [NB] MMAs of a batch of BS stages complete (commit)
-    uint64_t* aready = done + NB;    // [R]  group's 4 warps stored the stage's A tiles
-    uint64_t* accfull = aready + R;  // [2]  unit's MMAs complete (commit)
-    uint64_t* accempty = accfull + 2;  // [2] epilogue drained the accumulator
+    uint8_t* bring = smem;                              // [SB] activation stages (SW128 K-major)
+    uint8_t* wring = smem + SB * C::kBStageBytes;       // [SW] packed weight stages
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wring + SW * C::kWStageBytes);
+    uint64_t* wfull = bars;            // [SW] weights landed               (tx bytes)
+    uint64_t* wempty = wfull + SW;     // [SW] group's 4 warps read the stage (arrivals)
+    uint64_t* bfull = wempty + SW;     // [SB] activations landed           (tx bytes)
+    uint64_t* done = bfull + SB;       // [NB] MMAs of a batch of BS stages complete (commit)
+    uint64_t* aready = done + NB;      // [R]  group's 4 warps stored the stage's A tiles
+    uint64_t* accfull = aready + R;    // [2]  unit's MMAs complete (commit)
+    uint64_t* accempty = accfull + 2;  // [2]  epilogue drained the accumulator
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
 
     const uint32_t warp = warp_id_uniform();
@@ -536,7 +582,8 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     const uint32_t u_end = static_cast<uint32_t>((uint64_t)(blockIdx.x + 1) * p.units / gridDim.x);
 
     if (warp == C::kEpiWarp0 && lane == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < SW; ++i) mbar_init(&wfull[i], 1), mbar_init(&wempty[i], 4);
+        for (int i = 0; i < SB; ++i) mbar_init(&bfull[i], 1);
         for (int i = 0; i < NB; ++i) mbar_init(&done[i], 1);
         for (int i = 0; i < R; ++i) mbar_init(&aready[i], 4);
         for (int i = 0; i < 2; ++i) mbar_init(&accfull[i], 1), mbar_init(&accempty[i], 4);
@@ -556,24 +603,17 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     if (warp >= C::kProdWarp) {
         // ------------------------------------------------ producers
         // Weights are immutable for the duration of the call, so the first
-        // ring pass of weight tiles is requested BEFORE waiting for the
-        // preceding kernel (PDL): this CTA's HBM stream starts while the
-        // previous launch drains.  Activations (possibly written by that
-        // kernel) are requested only after griddepcontrol.wait.
+        // pass of the weight ring is requested BEFORE waiting for the
+        // preceding kernel (PDL, FPX_LINEAR_PDL=1); activations (possibly
+        // written by that kernel) only after griddepcontrol.wait.
         const uint32_t pw = warp - C::kProdWarp;
         const bool leader = lane == 0;
         const uint64_t pol_w = policy_evict_first();
         const uint64_t pol_b = policy_evict_last();
-        const uint32_t bytes = (p.dbg & 12u) == 0 ? C::kTxBytes
-                                                  : ((p.dbg & 8u) ? 0u : KS * C::kBBytes) +
-                                                        ((p.dbg & 4u) ? 0u : 2 * KS * (C::kHiBytes + C::kLoBytes));
-        // pass 0: first ring pass, weights only; pass 1: everything else
-#ifndef FPX_PDL_EARLY
-#define FPX_PDL_EARLY 1
-#endif
-        if (!FPX_PDL_EARLY) grid_dep_wait();
-        for (int pass = FPX_PDL_EARLY ? 0 : 1; pass < 2; ++pass) {
-            if (pass == 1 && FPX_PDL_EARLY) grid_dep_wait();
+        const uint32_t wtx = (p.dbg & 4u) ? 0u : C::kWTx;
+        const uint32_t btx = (p.dbg & 8u) ? 0u : C::kBTx;
+        for (int pass = 0; pass < 2; ++pass) {  // pass 0: first weight-ring pass only
+            if (pass == 1) grid_dep_wait();
             uint32_t si = 0;
             for (uint32_t u = u_begin; u < u_end; ++u) {
                 uint32_t mt, ch, s0, ns;
@@ -582,34 +622,42 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
                     if (si % C::kP != pw) continue;
                     const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
-                    const uint32_t st = si % S;
-                    uint8_t* sb = smem + st * C::kStageBytes;
-                    const bool first_pass = si < static_cast<uint32_t>(S);
-                    if (pass == 0 && !first_pass) break;
-                    if (pass == 1 && first_pass) {
-                        // weights already requested in pass 0
-                        if (leader && !(p.dbg & 8u)) tma_load_3d(sb, &act_map, 0, 0, k, &full[st], pol_b);
-                        continue;
-                    }
-                    if (!first_pass) {
-                        // stage si - S (same slot) is consumed once its batch's MMAs completed
-                        const uint32_t b = (si - S) / BS;
-                        if (leader) trace_mark(p, kTrDqDone3, si);
-                        wait_rec(p, &done[b % NB], (b / NB) & 1u, 1, si);
-                    }
-                    if (leader) {
-                        trace_mark(p, kTrProdIssue, si);
-                        // full boxes always land (OOB rows / k-tiles are zero-filled)
-                        mbar_arrive_expect_tx(&full[st], bytes);
-                        if (!(p.dbg & 4u)) {
-                            tma_load_3d(sb + C::kHiOff, &hi_map, 0, k, tr0, &full[st], pol_w);
-                            tma_load_3d(sb + C::kLoOff, &lo_map, 0, k, tr0, &full[st], pol_w);
+                    const bool w_first = si < static_cast<uint32_t>(SW);
+                    if (pass == 0 && !w_first) break;
+                    if (pass == 0 || !w_first) {
+                        // ---- weights: slot free once the group has read it
+                        const uint32_t ws = si % SW;
+                        if (!w_first) {
+                            if (leader) trace_mark(p, kTrDqDone3, si);
+                            wait_rec(p, &wempty[ws], ((si / SW) & 1u) ^ 1u, 1, si);
                         }
-                        if (pass == 1 && !(p.dbg & 8u)) tma_load_3d(sb, &act_map, 0, 0, k, &full[st], pol_b);
+                        if (leader) {
+                            trace_mark(p, kTrProdIssue, si);
+                            mbar_arrive_expect_tx(&wfull[ws], wtx);
+                            if (!(p.dbg & 4u)) {
+                                uint8_t* wb = wring + ws * C::kWStageBytes;
+                                tma_load_3d(wb, &hi_map, 0, k, tr0, &wfull[ws], pol_w);
+                                tma_load_3d(wb + C::kLoOff, &lo_map, 0, k, tr0, &wfull[ws], pol_w);
+                            }
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
+                    if (pass == 1) {
+                        // ---- activations: slot free once its batch's MMAs completed
+                        const uint32_t bs = si % SB;
+                        if (si >= static_cast<uint32_t>(SB)) {
+                            const uint32_t b = (si - SB) / BS;
+                            wait_rec(p, &done[b % NB], (b / NB) & 1u, 7, si);
+                        }
+                        if (leader) {
+                            mbar_arrive_expect_tx(&bfull[bs], btx);
+                            if (!(p.dbg & 8u))
+                                tma_load_3d(bring + bs * C::kBStageBytes, &act_map, 0, 0, k, &bfull[bs], pol_b);
+                        }
+                        __syncwarp();
+                    }
                 }
-                if (pass == 0 && si >= static_cast<uint32_t>(S)) break;
+                if (pass == 0 && si >= static_cast<uint32_t>(SW)) break;
             }
         }
     } else if (warp == C::kMmaWarp) {
@@ -627,11 +675,12 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
                 const uint32_t as = si % R;
                 if (leader) trace_mark(p, kTrMmaWait, si);
+                // aready implies the activation stage landed (the group waited bfull first)
                 wait_rec(p, &aready[as], (si / R) & 1u, 4, si);
                 tc_fence_after();
                 if (leader) trace_mark(p, kTrMmaGo, si);
                 const uint32_t a_tmem = tmem + as * KS * 32;
-                const uint64_t bdesc = umma_desc_sw128_kmajor(smem_u32(smem + (si % S) * C::kStageBytes));
+                const uint64_t bdesc = umma_desc_sw128_kmajor(smem_u32(bring + (si % SB) * C::kBStageBytes));
                 const uint32_t acc0 = ls > 0 ? 1u : 0u;  // the unit's first k-tile overwrites
                 if (!(p.dbg & 2u)) {
 #pragma unroll
@@ -749,24 +798,31 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             // this group's stages of the unit: si % G == g
             uint32_t ls = (g + G - si % G) % G;
             for (si += ls; ls < ns; ls += G, si += G) {
-                const uint32_t st = si % S, as = si % R;
-                const uint32_t sb = smem_u32(smem + st * C::kStageBytes);
+                const uint32_t ws = si % SW, as = si % R;
+                const uint32_t wb = smem_u32(wring + ws * C::kWStageBytes);
                 if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
-                wait_rec(p, &full[st], (si / S) & 1u, 3, si);
+                wait_rec(p, &wfull[ws], (si / SW) & 1u, 3, si);
                 if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);
-                uint32_t o[KS][2][16];
+                // all of the stage's packed words into registers, then hand the
+                // weight stage back to the producers
+                uint32_t w[KS][12];
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk)
+                    load_ktile_words<F>(wb + (r * KS + kk) * C::kHiBytes, wb + C::kLoOff + (r * KS + kk) * C::kLoBytes,
+                                        h, lane, w[kk]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&wempty[ws]);
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
                     // Rows of a missing second tile-row (odd tile_rows) and the
                     // FPX_LINEAR_DBG=1 no-math mode store zeros: every A-slot lane
                     // an MMA reads has been written by this CTA.
+                    uint32_t o0[16], o1[16];
                     if (valid && !(p.dbg & 1u)) {
-                        dequant_ktile_regs<F>(sb + C::kHiOff + (r * KS + kk) * C::kHiBytes,
-                                              sb + C::kLoOff + (r * KS + kk) * C::kLoBytes, h, lane, sc, o[kk][0],
-                                              o[kk][1]);
+                        dequant_words<F>(w[kk], h, sc, o0, o1);
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) o[kk][0][i] = 0u, o[kk][1][i] = 0u;
+                        for (int i = 0; i < 16; ++i) o0[i] = 0u, o1[i] = 0u;
                     }
                     if (kk == 0) {
                         // A slot `as` last held stage si - R: free once that stage's batch completed
@@ -778,11 +834,13 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                         if (q == 0 && lane == 0) trace_mark(p, kTrDqDone1, si);
                         tc_fence_after();
                     }
-                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32, o[kk][0]);
-                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32 + (16u << 16), o[kk][1]);
+                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32, o0);
+                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32 + (16u << 16), o1);
                 }
                 tmem_st_wait();
                 tc_fence_before();
+                // the MMA reads this stage's activations: make sure they landed
+                wait_rec(p, &bfull[si % SB], (si / SB) & 1u, 8, si);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&aready[as]);
                 if (q == 0 && lane == 0) trace_mark(p, kTrMmaAfull, si);
