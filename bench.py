@@ -113,6 +113,22 @@ class ClockSampler:
                 "window": "timed region + 0.3 s of the identical step directly after (nvidia-smi -lms 20)"}
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the decode kernel from the
+    committed ncu --set full capture (profiles/), bytes per launch, or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_decode_n16_summary.txt")))
+    if not files:
+        return None, None
+    txt = open(files[-1]).read()
+    rd = re.search(r"dram__bytes_read.sum = ([0-9.]+) Mbyte", txt)
+    wr = re.search(r"dram__bytes_write.sum = ([0-9.]+) Mbyte", txt)
+    if not (rd and wr):
+        return None, None
+    return round((float(rd.group(1)) + float(wr.group(1))) * 1e6), os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -276,6 +292,7 @@ def run_ours(args, rank, world, local):
     del W16, ref
 
     hbm, hbm_src = peaks()
+    traffic, traffic_src = ncu_traffic()
     value = world * nl * WEIGHT_BYTES / (total_ms * 1e-3) / 1e9
     achieved = WEIGHT_BYTES / (mean_launch_us * 1e-6) / 1e9
     res = {
@@ -290,7 +307,8 @@ def run_ours(args, rank, world, local):
         "us_per_launch": {str(n): round(v, 2) for n, v in per_n.items()},
         "timing": "CUDA events around CUDA-graph replays of the K timed steps (host launch overhead excluded)",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "traffic_source": f"{traffic_src} (N=16 launch, dram read+write bytes)" if traffic else None,
                      "peak_source": f"{hbm_src} MEASURED_PEAKS.json hbm_gbs" if hbm_src == "measured" else hbm_src,
                      "kernel": "fpx_linear_decode_kernel (mean device time per launch over the batch sweep)",
                      "algorithmic_bytes_per_launch": WEIGHT_BYTES},
