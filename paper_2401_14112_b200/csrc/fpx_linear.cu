@@ -77,6 +77,7 @@ struct KParams {
                   // 16 epilogue polls with back-off, 32 dequant A-slot polls with back-off
     unsigned long long* trace;  // optional per-stage clock trace of CTA 0 (fpx_debug_trace), else null
     volatile unsigned long long* prog;  // debug: mapped host memory, per (CTA, warp) current wait, else null
+    uint32_t pdl;  // launched with programmatic stream serialization (weights may be prefetched before the dependency wait)
 };
 
 // Debug (FPX_LINEAR_TRACE=3): record, in mapped host memory the host can read
@@ -526,8 +527,24 @@ struct GCfg {
     static constexpr int kLoOff = 2 * kKS * kHiBytes;
     static constexpr int kWStageBytes = (2 * kKS * (kHiBytes + kLoBytes) + 1023) / 1024 * 1024;
     static constexpr int kBStageBytes = (kKS * kBBytes + 1023) / 1024 * 1024;
-    static constexpr int kBStages = std::min(16, (kSmemBudget / 3) / kBStageBytes);
-    static constexpr int kWStages = std::min(16, (kSmemBudget - kBStages * kBStageBytes) / kWStageBytes);
+#ifndef FPX_DEC_SB
+#define FPX_DEC_SB 8
+#endif
+#ifndef FPX_DEC_SMEM_KB
+#define FPX_DEC_SMEM_KB 216
+#endif
+    // The activation ring only has to outlast a commit batch; everything else
+    // goes to the weight ring, whose depth (bytes in flight per SM) sets the
+    // sustainable HBM rate against the ~2.5 us loaded TMA latency.
+    static constexpr int kBStages = FPX_DEC_SB;
+    // A multiple of P: producer i issues stages i, i+P, ..., so each weight
+    // slot belongs to one producer, which therefore only ever waits on the
+    // consumption of its OWN previous stage in that slot.  With a slot shared
+    // by two producers, one producer could run two ring laps ahead of the
+    // other and its parity wait on wempty would alias an older phase
+    // (observed: corrupted barrier -> launch failure with an odd ring).
+    static constexpr int kWStages =
+        std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes) / kP * kP;
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
     static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
 #ifndef FPX_DEC_BS
@@ -540,6 +557,7 @@ struct GCfg {
     static constexpr uint32_t kWTx = 2 * kKS * (kHiBytes + kLoBytes);
     static constexpr uint32_t kBTx = kKS * kBBytes;
     static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
+    static_assert(kWStages % kP == 0, "weight slots must not be shared between producers");
     static_assert(NPAD <= 32, "decode kernel serves the small-batch regime");
 };
 
@@ -598,9 +616,14 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) trace_cta(p, 0);
-    grid_dep_launch();
+#ifndef FPX_PDL_LAUNCH_EARLY
+#define FPX_PDL_LAUNCH_EARLY 0
+#endif
+    if (FPX_PDL_LAUNCH_EARLY) grid_dep_launch();
 
-    if (warp >= C::kProdWarp) {
+    if (p.dbg & 256u) {
+        // FPX_LINEAR_DBG=256: launch + prologue + teardown only (bring-up)
+    } else if (warp >= C::kProdWarp) {
         // ------------------------------------------------ producers
         // Weights are immutable for the duration of the call, so the first
         // pass of the weight ring is requested BEFORE waiting for the
@@ -612,7 +635,9 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         const uint64_t pol_b = policy_evict_last();
         const uint32_t wtx = (p.dbg & 4u) ? 0u : C::kWTx;
         const uint32_t btx = (p.dbg & 8u) ? 0u : C::kBTx;
-        for (int pass = 0; pass < 2; ++pass) {  // pass 0: first weight-ring pass only
+        // Without PDL there is nothing to wait for: one pass, weights and
+        // activations of a stage issued together.
+        for (int pass = p.pdl ? 0 : 1; pass < 2; ++pass) {  // pass 0: first weight-ring pass only
             if (pass == 1) grid_dep_wait();
             uint32_t si = 0;
             for (uint32_t u = u_begin; u < u_end; ++u) {
@@ -622,12 +647,12 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
                     if (si % C::kP != pw) continue;
                     const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
-                    const bool w_first = si < static_cast<uint32_t>(SW);
+                    const bool w_first = p.pdl && si < static_cast<uint32_t>(SW);  // weights issued in pass 0
                     if (pass == 0 && !w_first) break;
                     if (pass == 0 || !w_first) {
                         // ---- weights: slot free once the group has read it
                         const uint32_t ws = si % SW;
-                        if (!w_first) {
+                        if (si >= static_cast<uint32_t>(SW)) {
                             if (leader) trace_mark(p, kTrDqDone3, si);
                             wait_rec(p, &wempty[ws], ((si / SW) & 1u) ^ 1u, 1, si);
                         }
@@ -779,22 +804,33 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         const int h = static_cast<int>(q & 1u);
         const uint32_t r = q >> 1;
         const uint32_t tq = tmem + ((32 * q) << 16);  // this warp's TMEM lane quarter
+        // Row scales are fetched one unit ahead: a dependent global load at
+        // every unit start would stall all groups at the same moment.
+        auto fetch_scales = [&](uint32_t uu, uint16_t (&raw)[2][2]) {
+            uint32_t mt_, ch_, s0_, ns_;
+            unit_stages<KS>(p, uu, mt_, ch_, s0_, ns_);
+            const uint32_t tr_ = 2 * mt_ + r;
+#pragma unroll
+            for (int lc = 0; lc < 2; ++lc)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+                    raw[lc][hf] = tr_ < p.tile_rows ? __ldg(&p.scales[tr_ * 64 + 16 * (2 * h + lc) + 8 * hf + lane / 4])
+                                                    : uint16_t(0);
+        };
+        uint16_t nxt[2][2] = {{0, 0}, {0, 0}};
+        if (u_begin < u_end) fetch_scales(u_begin, nxt);
         uint32_t si = 0;
         for (uint32_t u = u_begin; u < u_end; ++u) {
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
             const uint32_t tr = 2 * mt + r;
             const bool valid = tr < p.tile_rows;
-            uint32_t sc[2][2] = {{0, 0}, {0, 0}};
-            if (valid) {
+            uint32_t sc[2][2];
 #pragma unroll
-                for (int lc = 0; lc < 2; ++lc)
+            for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        const uint32_t row = tr * 64 + 16 * (2 * h + lc) + 8 * hf + lane / 4;
-                        sc[lc][hf] = row_scale_for<F, kHwCvt>(p.scales[row]);
-                    }
-            }
+                for (int hf = 0; hf < 2; ++hf) sc[lc][hf] = row_scale_for<F, kHwCvt>(nxt[lc][hf]);
+            if (u + 1 < u_end) fetch_scales(u + 1, nxt);
             // this group's stages of the unit: si % G == g
             uint32_t ls = (g + G - si % G) % G;
             for (si += ls; ls < ns; ls += G, si += G) {
@@ -852,6 +888,11 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace_cta(p, 7);
+    // PDL: the next launch may be scheduled once every CTA got here (its
+    // CTAs still need this CTA's shared memory / TMEM, so they start as
+    // these exit), overlapping its prologue and first weight loads with
+    // this launch's tail.
+    if (!FPX_PDL_LAUNCH_EARLY) grid_dep_launch();
     if (warp == C::kProdWarp) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
@@ -976,6 +1017,7 @@ cudaError_t launch_g(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return attr_err;
+    kq.pdl = pdl_enabled() ? 1u : 0u;
     return launch_pdl(kern, grid, C::kThreads, C::kSmemBytes, st, map, hi_map, lo_map, kq);
 }
 
@@ -993,12 +1035,11 @@ cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, in
     if (!classic && npad <= 32) {
         if (npad == 16) {
             if (ks == 1 && ng == 4) return launch_g<F, 16, 1, 4>(L, kp, grid, st);
-            if (ks == 2 && ng == 2) return launch_g<F, 16, 2, 2>(L, kp, grid, st);
-            if (ks == 4 && ng == 2) return launch_g<F, 16, 4, 2>(L, kp, grid, st);
+            if (ks == 2 && ng == 3) return launch_g<F, 16, 2, 3>(L, kp, grid, st);
+            if (ks == 2 && ng == 5) return launch_g<F, 16, 2, 5>(L, kp, grid, st);
             return launch_g<F, 16, 2, 4>(L, kp, grid, st);
         }
-        if (ks == 2 && ng == 2) return launch_g<F, 32, 2, 2>(L, kp, grid, st);
-        if (ks == 4 && ng == 2) return launch_g<F, 32, 4, 2>(L, kp, grid, st);
+        if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
         return launch_g<F, 32, 2, 4>(L, kp, grid, st);
     }
     switch (npad) {
