@@ -98,7 +98,7 @@ constexpr size_t kLinearCounterBytes = 64 * 1024;  // split-K arrival counters (
 // per-CTA timeline).  FPX_LINEAR_TRACE=1: one buffer, cleared per call.
 // FPX_LINEAR_TRACE=2: calls alternate between two buffers that are cleared
 // only on allocation, so two consecutive launches can be compared.
-constexpr size_t kTraceWords = 16 * 512;
+constexpr size_t kTraceWords = 32 * 512;
 unsigned long long* g_trace = nullptr;
 unsigned long long* debug_trace_buffer() {
     static int mode = [] {

@@ -102,12 +102,15 @@ __device__ __forceinline__ void trace_mark(const KParams& p, int ev, uint32_t si
 }
 
 // Whole-grid timeline (globaltimer ns): per CTA slot e (0 = start after the
-// prologue, 1..6 = unit ends, 7 = exit), at trace[12*512 + cta*8 + e].
+// prologue, 1..6 = unit ends, 7 = thread 0 at the final barrier, 8 = producer
+// done, 9 = MMA issuer done, 10 = de-quantiser warp 0 done, 11 = epilogue
+// done, 12 = teardown (all warps done), 13 = TMEM freed), at
+// trace[12*512 + cta*16 + e].
 __device__ __forceinline__ void trace_cta(const KParams& p, uint32_t e) {
-    if (p.trace != nullptr && blockIdx.x < 256 && e < 8) {
+    if (p.trace != nullptr && blockIdx.x < 256 && e < 16) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[12 * kTraceStages + blockIdx.x * 8 + e] = t;
+        p.trace[12 * kTraceStages + blockIdx.x * 16 + e] = t;
     }
 }
 
@@ -616,10 +619,9 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) trace_cta(p, 0);
-#ifndef FPX_PDL_LAUNCH_EARLY
-#define FPX_PDL_LAUNCH_EARLY 0
-#endif
-    if (FPX_PDL_LAUNCH_EARLY) grid_dep_launch();
+    // PDL only: let the next launch be scheduled (its CTAs still need this
+    // CTA's shared memory / TMEM, so they start as these exit).
+    if (p.pdl) grid_dep_launch();
 
     if (p.dbg & 256u) {
         // FPX_LINEAR_DBG=256: launch + prologue + teardown only (bring-up)
@@ -737,7 +739,10 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             tc_fence_after();
             const uint32_t m = mt * kTileM + row_l;
             const bool row_ok = m < p.rows_p;
-            float* part = p.ws + (static_cast<size_t>(mt) * p.split + ch) * NPAD * kTileM;
+            // split-K partials: [unit][col/4][row][4] fp32 -- a lane's 4 columns
+            // are one 16-byte vector and a warp's 32 rows are contiguous, so the
+            // stores here and the loads of the reduction are coalesced float4s
+            float* part = p.ws + (static_cast<size_t>(mt) * p.split + ch) * kTileM * NPAD + row_l * 4;
             const uint32_t tacc = tmem + ((32 * q) << 16) + C::kAccCol0 + ab * NPAD;
 #pragma unroll
             for (uint32_t c0 = 0; c0 < NPAD; c0 += 16) {
@@ -749,18 +754,20 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K chunk contributes zero
                 }
-                if (c0 < p.n) {
+                if (p.split == 1) {
+                    if (c0 < p.n && row_ok) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t col = c0 + j;
-                        if (col < p.n) {
-                            if (p.split == 1) {
-                                if (row_ok) p.c[static_cast<size_t>(col) * p.ldc + m] = __uint_as_float(v[j]);
-                            } else {
-                                part[static_cast<size_t>(col) * kTileM + row_l] = __uint_as_float(v[j]);
-                            }
-                        }
+                        for (int j = 0; j < 16; ++j)
+                            if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = __uint_as_float(v[j]);
                     }
+                } else if (c0 < p.n) {
+                    // columns >= n hold exact zeros (zero-filled activations)
+                    // kept in L2 (evict_last) against the evict_first weight stream:
+                    // the last arriver reads them back on the launch's tail
+                    const uint64_t pol_keep = policy_evict_last();
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        st_global_v4_hint(part + ((c0 + j) / 4) * kTileM * 4, v[j], v[j + 1], v[j + 2], v[j + 3], pol_keep);
                 }
             }
             tc_fence_before();
@@ -770,29 +777,48 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             if (p.split > 1) {
                 __threadfence();
                 __syncwarp();
+                if (q == 0 && lane == 0) trace_cta(p, 14);
                 uint32_t old = 0;
                 if (lane == 0) old = atomicAdd(&p.counters[mt * 4 + q], 1u);
                 old = __shfl_sync(0xffffffffu, old, 0);
+                if (q == 0 && lane == 0) trace_cta(p, 15);
                 if (old == p.split - 1) {
-                    // last arriver: C = ((P0 + P1) + P2) + ... in chunk order
+                    // last arriver: C = ((0 + P0) + P1) + ... in chunk order.  This
+                    // reduction can sit on the launch's tail and is L2-latency
+                    // bound: loads of two chunks x four 4-column slices (8 x 16 B)
+                    // are in flight per round trip.
                     __threadfence();
-                    const float* base = p.ws + static_cast<size_t>(mt) * p.split * NPAD * kTileM + row_l;
-                    for (uint32_t c0 = 0; c0 < p.n; c0 += 16) {
-                        float acc[16];
+                    if (q == 0 && lane == 0) trace_cta(p, 10);
+                    const float* base = p.ws + static_cast<size_t>(mt) * p.split * kTileM * NPAD + row_l * 4;
+                    const size_t cstride = static_cast<size_t>(kTileM) * NPAD;
+                    const uint64_t pol_drop = policy_evict_first();
+                    // one L2 round trip per 4-column slice: all chunks' loads in flight
+                    constexpr uint32_t kMaxChunks = NPAD <= 16 ? 10 : 6;  // register budget
+                    for (uint32_t c0 = 0; c0 < p.n; c0 += 4) {
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (uint32_t cb = 0; cb < p.split; cb += kMaxChunks) {
+                            float4 t[kMaxChunks];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
-                        for (uint32_t cc = 0; cc < p.split; ++cc) {
-                            const float* pc = base + (static_cast<size_t>(cc) * NPAD + c0) * kTileM;
+                            for (uint32_t u = 0; u < kMaxChunks; ++u)
+                                if (cb + u < p.split)
+                                    t[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride + (c0 / 4) * kTileM * 4, pol_drop);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (c0 + j < p.n) acc[j] += __ldcg(pc + j * kTileM);
+                            for (uint32_t u = 0; u < kMaxChunks; ++u)
+                                if (cb + u < p.split) {
+                                    acc.x += t[u].x;
+                                    acc.y += t[u].y;
+                                    acc.z += t[u].z;
+                                    acc.w += t[u].w;
+                                }
                         }
                         if (row_ok) {
+                            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = acc[j];
+                            for (int j = 0; j < 4; ++j)
+                                if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = a4[j];
                         }
                     }
+                    if (q == 0 && lane == 0) trace_cta(p, 8);
                     if (lane == 0) p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
                 }
             }
@@ -885,17 +911,18 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         }
     }
 
+    if (lane == 0) {
+        if (warp == C::kMmaWarp) trace_cta(p, 9);
+        else if (warp == C::kEpiWarp0) trace_cta(p, 11);
+    }
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace_cta(p, 7);
-    // PDL: the next launch may be scheduled once every CTA got here (its
-    // CTAs still need this CTA's shared memory / TMEM, so they start as
-    // these exit), overlapping its prologue and first weight loads with
-    // this launch's tail.
-    if (!FPX_PDL_LAUNCH_EARLY) grid_dep_launch();
     if (warp == C::kProdWarp) {
         tc_fence_after();
+        if (lane == 0) trace_cta(p, 12);  // teardown: every warp of the CTA is done
         tmem_dealloc<kTmemCols>(tmem);
+        if (lane == 0) trace_cta(p, 13);  // after TMEM dealloc
     }
 }
 

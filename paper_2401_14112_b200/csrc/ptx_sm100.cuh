@@ -150,6 +150,22 @@ FPX_DEV uint64_t policy_evict_last() {
     return p;
 }
 
+// 16-byte global store / L2 load with an L2 cache-eviction policy.
+FPX_DEV void st_global_v4_hint(void* ptr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(a), "r"(b), "r"(c),
+                 "r"(d), "l"(policy)
+                 : "memory");
+}
+
+FPX_DEV float4 ld_global_cg_v4_hint(const void* ptr, uint64_t policy) {
+    float4 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(ptr), "l"(policy)
+                 : "memory");
+    return v;
+}
+
 // 1-D bulk copy global -> shared, completion on an mbarrier (bytes % 16 == 0).
 FPX_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
     asm volatile(

@@ -21,9 +21,9 @@ for _ in range(3):
     st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, fmt.exp_bits, fmt.man_bits, act.data_ptr(), K, n,
                       out.data_ptr(), M, split, ws.data_ptr(), ws.numel(), s)
 torch.cuda.synchronize()
-buf = np.zeros(16 * 512, np.uint64)
+buf = np.zeros(32 * 512, np.uint64)
 assert L.fpx_debug_trace(buf.ctypes.data, buf.size) == 0
-tr = buf.reshape(16, 512).astype(np.int64)
+tr = buf.reshape(32, 512).astype(np.int64)
 ev = {"pwait": 9, "prod": 0, "start": 1, "full": 2, "dq0": 3, "slot": 7, "ready": 4, "mwait": 10, "mgo": 11, "mma": 5}
 t0 = tr[0][tr[0] > 0].min()
 ns = int((tr[0] > 0).sum())
@@ -43,7 +43,7 @@ print("mean MMA-thread loop body (issued -> next wait): %.3f us" % np.nanmean([f
 print("mean producer loop body (issue -> next pre-wait): %.3f us" % np.nanmean([f('pwait', si + 1) - f('prod', si) for si in range(ns - 1)]))
 
 # whole-grid timeline (globaltimer, ns)
-cta = buf[12 * 512: 12 * 512 + 256 * 8].reshape(256, 8).astype(np.int64)
+cta = buf[12 * 512: 12 * 512 + 256 * 16].reshape(256, 16).astype(np.int64)
 live = cta[:, 0] > 0
 cta = cta[live]
 base = cta[:, 0].min()

@@ -16,11 +16,11 @@ for _ in range(4):  # calls 0..3 -> buffers 0,1,0,1: the last two launches are c
     st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, fmt.exp_bits, fmt.man_bits, act.data_ptr(), K, n,
                       out.data_ptr(), M, split, ws.data_ptr(), ws.numel(), s)
 torch.cuda.synchronize()
-buf = np.zeros(2 * 16 * 512, np.uint64)
+buf = np.zeros(2 * 32 * 512, np.uint64)
 assert L.fpx_debug_trace(buf.ctypes.data, buf.size) == 0
 tl = []
 for b in range(2):
-    c = buf[b * 8192 + 12 * 512: b * 8192 + 12 * 512 + 256 * 8].reshape(256, 8).astype(np.int64)
+    c = buf[b * 16384 + 12 * 512: b * 16384 + 12 * 512 + 256 * 16].reshape(256, 16).astype(np.int64)
     tl.append(c[c[:, 0] > 0])
 base = tl[0][:, 0].min()
 for b, c in enumerate(tl):
