@@ -382,7 +382,8 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
     float* part = reinterpret_cast<float*>(ws + lay.part_off);
     const char* g = std::getenv("FPX_LINEAR_GRID");
     const int grid = g ? std::atoi(g) : num_sms();
-    for (uint32_t n0 = 0; n0 < n; n0 += 256) {
+    const uint32_t chunk = 256u;  // widest accumulator of the fused kernels
+    for (uint32_t n0 = 0; n0 < n; n0 += chunk) {
         LinearLaunch L{};
         L.fmt = fmt;
         L.s_hi = streams[0];
@@ -392,7 +393,7 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
         L.cols_p = cols_p;
         L.act = a + static_cast<size_t>(n0) * cols_p;
         L.lda = cols_p;
-        L.n = (n - n0) < 256 ? (n - n0) : 256;
+        L.n = (n - n0) < chunk ? (n - n0) : chunk;
         L.c = c + static_cast<size_t>(n0) * ldc;
         L.ldc = ldc;
         L.split = split_k;

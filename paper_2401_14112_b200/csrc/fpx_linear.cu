@@ -539,7 +539,7 @@ struct GCfg {
     // The activation ring only has to outlast a commit batch; everything else
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
-    static constexpr int kBStages = FPX_DEC_SB;
+    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 4 : 3);
     // A multiple of P: producer i issues stages i, i+P, ..., so each weight
     // slot belongs to one producer, which therefore only ever waits on the
     // consumption of its OWN previous stage in that slot.  With a slot shared
@@ -561,7 +561,7 @@ struct GCfg {
     static constexpr uint32_t kBTx = kKS * kBBytes;
     static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
     static_assert(kWStages % kP == 0, "weight slots must not be shared between producers");
-    static_assert(NPAD <= 32, "decode kernel serves the small-batch regime");
+    static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
 
 // Stage-granular unit range: chunk c of a 128-row tile covers stages
@@ -1010,13 +1010,23 @@ cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
     auto kern = fpx_linear_kernel<F, NPAD, KS_, NG_>;
     CUtensorMap map;
     if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
+    // NPAD = 256 (single accumulator buffer): intermittent wrong results were
+    // measured at split 9 (not understood yet); split is capped at 2 -- the
+    // default for this width -- and each CTA runs one unit.  The cap depends
+    // on N only, so tile-row shards still reproduce the unsharded rows.
+    KParams kq = kp;
+    if (C::kAccBufs == 1 && kq.split > 2) {
+        kq.split = 2;
+        kq.units = (kp.rows_p + kTileM - 1) / kTileM * 2;
+    }
+    if (C::kAccBufs == 1) grid = static_cast<int>(kq.units);
     static std::once_flag attr_once;  // per instantiation (the attribute is per function)
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(map, kp);
+    kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(map, kq);
     return cudaGetLastError();
 }
 
@@ -1060,15 +1070,23 @@ cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, in
     const char* kname = std::getenv("FPX_LINEAR_KERNEL");
     const bool classic = kname != nullptr && std::strcmp(kname, "classic") == 0;
     if (!classic && npad <= 32) {
-        if (npad == 16) {
+        if (npad <= 16) {
             if (ks == 1 && ng == 4) return launch_g<F, 16, 1, 4>(L, kp, grid, st);
             if (ks == 2 && ng == 3) return launch_g<F, 16, 2, 3>(L, kp, grid, st);
             if (ks == 2 && ng == 5) return launch_g<F, 16, 2, 5>(L, kp, grid, st);
             return launch_g<F, 16, 2, 4>(L, kp, grid, st);
         }
-        if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
-        return launch_g<F, 32, 2, 4>(L, kp, grid, st);
+        if (npad == 32) {
+            if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
+            return launch_g<F, 32, 2, 4>(L, kp, grid, st);
+        }
     }
+    // N > 32: the single-issuer kernel (measured faster there than the decode
+    // kernel with its NPAD-wide accumulators and activation ring);
+    // FPX_LINEAR_KERNEL=decode routes N <= 128 through the decode kernel.
+    const bool decode = kname != nullptr && std::strcmp(kname, "decode") == 0;
+    if (decode && npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
+    if (decode && npad == 128) return launch_g<F, 128, 2, 4>(L, kp, grid, st);
     switch (npad) {
         case 16: return launch_t<F, 16, 2, 3>(L, kp, grid, st);
         case 32: return launch_t<F, 32, 2, 3>(L, kp, grid, st);
