@@ -691,7 +691,12 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         // ------------------------------------------------ MMA issuer
         constexpr uint32_t idesc = umma_idesc_f16(kTileM, NPAD);
         const bool leader = lane == 0;
+        // ring positions advance incrementally (no divisions on this
+        // single-issue critical path)
         uint32_t si = 0, lu = 0;
+        uint32_t as = 0, aph = 0;   // A slot and its phase parity
+        uint32_t bsl = 0;           // activation slot
+        uint32_t nb = 0, nbs = 0;   // stages in the open commit batch, batch barrier slot
         for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
@@ -700,14 +705,13 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             tc_fence_after();
             const uint32_t d_tmem = tmem + C::kAccCol0 + ab * NPAD;
             for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
-                const uint32_t as = si % R;
                 if (leader) trace_mark(p, kTrMmaWait, si);
                 // aready implies the activation stage landed (the group waited bfull first)
-                wait_rec(p, &aready[as], (si / R) & 1u, 4, si);
+                wait_rec(p, &aready[as], aph, 4, si);
                 tc_fence_after();
                 if (leader) trace_mark(p, kTrMmaGo, si);
                 const uint32_t a_tmem = tmem + as * KS * 32;
-                const uint64_t bdesc = umma_desc_sw128_kmajor(smem_u32(bring + (si % SB) * C::kBStageBytes));
+                const uint64_t bdesc = umma_desc_sw128_kmajor(smem_u32(bring + bsl * C::kBStageBytes));
                 const uint32_t acc0 = ls > 0 ? 1u : 0u;  // the unit's first k-tile overwrites
                 if (!(p.dbg & 2u)) {
 #pragma unroll
@@ -718,12 +722,18 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                                              bdesc + static_cast<uint64_t>((kk * C::kBBytes + ks * 32) >> 4), idesc,
                                              (kk > 0 || ks > 0) ? 1u : acc0);
                 }
-                if ((si + 1) % BS == 0) umma_commit_warp(&done[(si / BS) % NB]);
+                if (++nb == static_cast<uint32_t>(BS)) {
+                    umma_commit_warp(&done[nbs]);
+                    nb = 0;
+                    nbs = (nbs + 1 == static_cast<uint32_t>(NB)) ? 0u : nbs + 1;
+                }
                 if (leader) trace_mark(p, kTrMmaIssued, si);
+                if (++as == static_cast<uint32_t>(R)) as = 0, aph ^= 1u;
+                if (++bsl == static_cast<uint32_t>(SB)) bsl = 0;
             }
             umma_commit_warp(&accfull[ab]);
         }
-        if (si % BS != 0) umma_commit_warp(&done[(si / BS) % NB]);  // final partial batch
+        if (nb != 0) umma_commit_warp(&done[nbs]);  // final partial batch
     } else if (warp >= C::kEpiWarp0) {
         // ------------------------------------------------ epilogue
         grid_dep_wait();  // C / partials / counters may still be in use by the preceding kernel
