@@ -257,7 +257,16 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // The CTA owns all 512 TMEM columns of its SM (1 CTA/SM), so the
+    // allocation can only start at lane 0 / column 0.  Using the constant
+    // keeps every TMEM operand of the MMA loop in uniform registers
+    // regardless of how the compiler judges the shared-memory load.
+#ifdef FPX_TMEM_CONST
+    if (*tmem_slot != 0u) __trap();
+    constexpr uint32_t tmem = 0;
+#else
     const uint32_t tmem = *tmem_slot;
+#endif
 
     if (warp == C::kProdWarp) {
         // ------------------------------------------------ producer
@@ -576,6 +585,59 @@ __device__ __forceinline__ void unit_stages(const KParams& p, uint32_t u, uint32
     ns = ((ch + 1) * nst) / p.split - s0;
 }
 
+// Deferred last-unit split-K reductions, by every thread of the CTA: items
+// are (pending lane quarter, row, 4-column slice), rows fastest, so a warp
+// reads 512 contiguous bytes per chunk.  Same chunk order as the epilogue's
+// in-loop reduction, hence bit-identical results.
+template <int NPAD>
+__device__ __forceinline__ void final_split_reduce(const KParams& p, const uint32_t* final_red, uint32_t nthreads) {
+    uint32_t npend = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) npend += final_red[i] != 0u ? 1u : 0u;
+    const uint32_t nsl = (p.n + 3) / 4;
+    const uint32_t items = npend * 32 * nsl;
+    const size_t cstride = static_cast<size_t>(kTileM) * NPAD;
+    const uint64_t pol_drop = policy_evict_first();
+    for (uint32_t it = threadIdx.x; it < items; it += nthreads) {
+        const uint32_t rl = it & 31u, rest = it >> 5;
+        const uint32_t sl = rest % nsl, pi = rest / nsl;
+        uint32_t tq = 0, seen = 0;  // the pi-th pending quarter (tile * 4 + quarter)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t f = final_red[i];
+            if (f != 0u) {
+                if (seen == pi) tq = (f - 1) * 4 + i;
+                ++seen;
+            }
+        }
+        const uint32_t mt = tq >> 2, row_l = 32 * (tq & 3u) + rl;
+        const float* base = p.ws + static_cast<size_t>(mt) * p.split * cstride + sl * kTileM * 4 + row_l * 4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        constexpr uint32_t kInFlight = 12;
+        for (uint32_t cb = 0; cb < p.split; cb += kInFlight) {
+            float4 t[kInFlight];
+#pragma unroll
+            for (uint32_t u = 0; u < kInFlight; ++u)
+                if (cb + u < p.split) t[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride, pol_drop);
+#pragma unroll
+            for (uint32_t u = 0; u < kInFlight; ++u)
+                if (cb + u < p.split) {
+                    acc.x += t[u].x;
+                    acc.y += t[u].y;
+                    acc.z += t[u].z;
+                    acc.w += t[u].w;
+                }
+        }
+        const uint32_t m = mt * kTileM + row_l;
+        if (m < p.rows_p) {
+            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (4 * sl + j < p.n) p.c[static_cast<size_t>(4 * sl + j) * p.ldc + m] = a4[j];
+        }
+    }
+}
+
 template <int F, int NPAD, int KS_, int G_>
 __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     fpx_linear_decode_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap hi_map,
@@ -596,6 +658,10 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     uint64_t* accfull = aready + R;    // [2]  unit's MMAs complete (commit)
     uint64_t* accempty = accfull + 2;  // [2]  epilogue drained the accumulator
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+    // [4] per epilogue lane quarter: 1 + tile of a deferred last-unit
+    // reduction, or 0.  A separate static array: stores next to tmem_slot
+    // cost the MMA loop its uniform-register TMEM operands (ptxas).
+    __shared__ uint32_t final_red[4];
 
     const uint32_t warp = warp_id_uniform();
     const uint32_t lane = lane_id();
@@ -617,7 +683,16 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // The CTA owns all 512 TMEM columns of its SM (1 CTA/SM), so the
+    // allocation can only start at lane 0 / column 0.  Using the constant
+    // keeps every TMEM operand of the MMA loop in uniform registers
+    // regardless of how the compiler judges the shared-memory load.
+#ifdef FPX_TMEM_CONST
+    if (*tmem_slot != 0u) __trap();
+    constexpr uint32_t tmem = 0;
+#else
     const uint32_t tmem = *tmem_slot;
+#endif
     if (threadIdx.x == 0) trace_cta(p, 0);
     // PDL only: let the next launch be scheduled (its CTAs still need this
     // CTA's shared memory / TMEM, so they start as these exit).
@@ -739,6 +814,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         grid_dep_wait();  // C / partials / counters may still be in use by the preceding kernel
         const uint32_t q = warp & 3u;
         const uint32_t row_l = 32 * q + lane;
+        if (lane == 0) final_red[q] = 0u;  // read only after the final __syncthreads
         uint32_t lu = 0;
         for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
             uint32_t mt, ch, s0, ns;
@@ -792,7 +868,16 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 if (lane == 0) old = atomicAdd(&p.counters[mt * 4 + q], 1u);
                 old = __shfl_sync(0xffffffffu, old, 0);
                 if (q == 0 && lane == 0) trace_cta(p, 15);
-                if (old == p.split - 1) {
+                if (old == p.split - 1 && u + 1 == u_end) {
+                    // The CTA's last unit: its reduction would sit on the launch's
+                    // tail with 128 threads and one L2 round trip per 4-column
+                    // slice; defer it to all warps of the CTA (below).
+                    __threadfence();  // acquire side of the counter (the other chunks' partials)
+                    if (lane == 0) {
+                        final_red[q] = mt + 1;
+                        p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
+                    }
+                } else if (old == p.split - 1) {
                     // last arriver: C = ((0 + P0) + P1) + ... in chunk order.  This
                     // reduction can sit on the launch's tail and is L2-latency
                     // bound: loads of two chunks x four 4-column slices (8 x 16 B)
@@ -934,6 +1019,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         tmem_dealloc<kTmemCols>(tmem);
         if (lane == 0) trace_cta(p, 13);  // after TMEM dealloc
     }
+    if (p.split > 1) final_split_reduce<NPAD>(p, final_red, C::kThreads);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -33,6 +33,22 @@ def test_library_is_sm100a_only():
         assert mnemonic in sass, mnemonic
 
 
+def test_decode_mma_operands_stay_uniform():
+    """Every UTCHMMA operand of the decode kernels must come from uniform
+    registers: a TMEM / descriptor value ptxas cannot prove warp-uniform is
+    moved with an ELECT + R2UR.BROADCAST loop per MMA, which was measured to
+    cost ~3 us per launch.  ptxas's judgement is fragile (e.g. plain stores
+    next to the TMEM address slot in shared memory flip it), so guard it."""
+    import re
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    fns = re.split(r"\n\s+Function : ", sass)[1:]
+    decode = [f for f in fns if "fpx_linear_decode_kernel" in f.split("\n")[0]]
+    assert decode
+    for f in decode:
+        assert "UTCHMMA" in f
+        assert "R2UR.BROADCAST" not in f, f.split("\n")[0]
+
+
 def test_format_helpers_match_oracle(oracle):
     L = _lib.load()
     for e in range(0, 7):
