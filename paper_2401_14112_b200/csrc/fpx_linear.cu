@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
 //    inside the asm.
 //
 // Pipeline (one persistent CTA per SM, units = (128-row tile, K chunk)):
-//  producers (P warps) --TMA--> weight ring (SW stages: KS k-tiles of packed
+//  producers (one weight warp, one activation warp) --TMA--> weight ring (SW stages: KS k-tiles of packed
 //    weights for the unit's 2 tile-rows) and activation ring (SB stages: KS
 //    activation k-tiles, the MMA's B operand)
 //  de-quantiser groups (G x 4 warps; stage si -> group si % G): LDS the
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
 // zero-filled by TMA (weights and activations), contributing exact zeros.
 //
 // Warps: 0 .. 4G-1 de-quantisers (group w/4, TMEM lane quarter w%4),
-// 4G .. 4G+3 epilogue (quarter w%4), 4G+4 MMA issuer, 4G+5 .. 4G+4+P TMA
-// producers (the first also allocates TMEM).
+// 4G .. 4G+3 epilogue (quarter w%4), 4G+4 MMA issuer, 4G+5 weight producer
+// (also allocates TMEM), 4G+6 activation producer.
 template <int F, int NPAD, int KS_, int G_, int P_ = 2>
 struct GCfg {
     static constexpr int kKS = KS_;
@@ -549,14 +549,10 @@ struct GCfg {
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
     static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 4 : 3);
-    // A multiple of P: producer i issues stages i, i+P, ..., so each weight
-    // slot belongs to one producer, which therefore only ever waits on the
-    // consumption of its OWN previous stage in that slot.  With a slot shared
-    // by two producers, one producer could run two ring laps ahead of the
-    // other and its parity wait on wempty would alias an older phase
-    // (observed: corrupted barrier -> launch failure with an odd ring).
+    // Each ring has exactly one producer warp, which only ever waits on the
+    // consumption of its own previous use of a slot (no parity aliasing).
     static constexpr int kWStages =
-        std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes) / kP * kP;
+        std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes);
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
     static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
 #ifndef FPX_DEC_BS
@@ -569,7 +565,7 @@ struct GCfg {
     static constexpr uint32_t kWTx = 2 * kKS * (kHiBytes + kLoBytes);
     static constexpr uint32_t kBTx = kKS * kBBytes;
     static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
-    static_assert(kWStages % kP == 0, "weight slots must not be shared between producers");
+    static_assert(kP == 2, "one weight producer warp and one activation producer warp");
     static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
 
@@ -700,68 +696,73 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
 
     if (p.dbg & 256u) {
         // FPX_LINEAR_DBG=256: launch + prologue + teardown only (bring-up)
-    } else if (warp >= C::kProdWarp) {
-        // ------------------------------------------------ producers
-        // Weights are immutable for the duration of the call, so the first
-        // pass of the weight ring is requested BEFORE waiting for the
-        // preceding kernel (PDL, FPX_LINEAR_PDL=1); activations (possibly
-        // written by that kernel) only after griddepcontrol.wait.
-        const uint32_t pw = warp - C::kProdWarp;
+    } else if (warp == C::kProdWarp) {
+        // ------------------------------------------------ weight producer
+        // Weights only, every stage: its sole throttle is the weight ring
+        // (slots come back as soon as a group has the words in registers),
+        // so up to SW stages of HBM reads stay in flight.  Sharing a warp with
+        // the activation loads -- whose slots come back only with MMA
+        // completion -- capped the weight prefetch depth at the activation
+        // ring's.  Weights are immutable during the call, so under PDL they
+        // are requested BEFORE waiting for the preceding kernel.
         const bool leader = lane == 0;
         const uint64_t pol_w = policy_evict_first();
-        const uint64_t pol_b = policy_evict_last();
         const uint32_t wtx = (p.dbg & 4u) ? 0u : C::kWTx;
-        const uint32_t btx = (p.dbg & 8u) ? 0u : C::kBTx;
-        // Without PDL there is nothing to wait for: one pass, weights and
-        // activations of a stage issued together.
-        for (int pass = p.pdl ? 0 : 1; pass < 2; ++pass) {  // pass 0: first weight-ring pass only
-            if (pass == 1) grid_dep_wait();
-            uint32_t si = 0;
-            for (uint32_t u = u_begin; u < u_end; ++u) {
-                uint32_t mt, ch, s0, ns;
-                unit_stages<KS>(p, u, mt, ch, s0, ns);
-                const int32_t tr0 = static_cast<int32_t>(2 * mt);
-                for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
-                    if (si % C::kP != pw) continue;
-                    const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
-                    const bool w_first = p.pdl && si < static_cast<uint32_t>(SW);  // weights issued in pass 0
-                    if (pass == 0 && !w_first) break;
-                    if (pass == 0 || !w_first) {
-                        // ---- weights: slot free once the group has read it
-                        const uint32_t ws = si % SW;
-                        if (si >= static_cast<uint32_t>(SW)) {
-                            if (leader) trace_mark(p, kTrDqDone3, si);
-                            wait_rec(p, &wempty[ws], ((si / SW) & 1u) ^ 1u, 1, si);
-                        }
-                        if (leader) {
-                            trace_mark(p, kTrProdIssue, si);
-                            mbar_arrive_expect_tx(&wfull[ws], wtx);
-                            if (!(p.dbg & 4u)) {
-                                uint8_t* wb = wring + ws * C::kWStageBytes;
-                                tma_load_3d(wb, &hi_map, 0, k, tr0, &wfull[ws], pol_w);
-                                tma_load_3d(wb + C::kLoOff, &lo_map, 0, k, tr0, &wfull[ws], pol_w);
-                            }
-                        }
-                        __syncwarp();
-                    }
-                    if (pass == 1) {
-                        // ---- activations: slot free once its batch's MMAs completed
-                        const uint32_t bs = si % SB;
-                        if (si >= static_cast<uint32_t>(SB)) {
-                            const uint32_t b = (si - SB) / BS;
-                            wait_rec(p, &done[b % NB], (b / NB) & 1u, 7, si);
-                        }
-                        if (leader) {
-                            mbar_arrive_expect_tx(&bfull[bs], btx);
-                            if (!(p.dbg & 8u))
-                                tma_load_3d(bring + bs * C::kBStageBytes, &act_map, 0, 0, k, &bfull[bs], pol_b);
-                        }
-                        __syncwarp();
+        uint32_t si = 0, ws = 0, wph = 0;  // stage, weight slot, slot parity
+        for (uint32_t u = u_begin; u < u_end; ++u) {
+            uint32_t mt, ch, s0, ns;
+            unit_stages<KS>(p, u, mt, ch, s0, ns);
+            const int32_t tr0 = static_cast<int32_t>(2 * mt);
+            for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
+                const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
+                // slot free once the group that read it (stage si - SW) released it
+                if (si >= static_cast<uint32_t>(SW)) wait_rec(p, &wempty[ws], wph ^ 1u, 1, si);
+                if (leader) {
+                    trace_mark(p, kTrProdIssue, si);
+                    mbar_arrive_expect_tx(&wfull[ws], wtx);
+                    if (!(p.dbg & 4u)) {
+                        uint8_t* wb = wring + ws * C::kWStageBytes;
+                        tma_load_3d(wb, &hi_map, 0, k, tr0, &wfull[ws], pol_w);
+                        tma_load_3d(wb + C::kLoOff, &lo_map, 0, k, tr0, &wfull[ws], pol_w);
                     }
                 }
-                if (pass == 0 && si >= static_cast<uint32_t>(SW)) break;
+                __syncwarp();
+                if (++ws == static_cast<uint32_t>(SW)) ws = 0, wph ^= 1u;
             }
         }
+    } else if (warp == C::kProdWarp + 1) {
+        // ------------------------------------------------ activation producer
+        // Activations may be written by the preceding kernel: wait for it.
+        grid_dep_wait();
+        const bool leader = lane == 0;
+        const uint64_t pol_b = policy_evict_last();
+        const uint32_t btx = (p.dbg & 8u) ? 0u : C::kBTx;
+        uint32_t si = 0, bs = 0;
+        uint32_t b = 0, bb = 0, nbs = 0, nph = 0;  // batch releasing slot bs: stage si - SB
+        for (uint32_t u = u_begin; u < u_end; ++u) {
+            uint32_t mt, ch, s0, ns;
+            unit_stages<KS>(p, u, mt, ch, s0, ns);
+            for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
+                const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
+                if (si >= static_cast<uint32_t>(SB)) {
+                    // stage si - SB belongs to MMA batch b = (si - SB) / BS
+                    wait_rec(p, &done[nbs], nph, 7, si);
+                    if (++bb == static_cast<uint32_t>(BS)) {
+                        bb = 0;
+                        ++b;
+                        if (++nbs == static_cast<uint32_t>(NB)) nbs = 0, nph ^= 1u;
+                    }
+                }
+                if (leader) {
+                    mbar_arrive_expect_tx(&bfull[bs], btx);
+                    if (!(p.dbg & 8u))
+                        tma_load_3d(bring + bs * C::kBStageBytes, &act_map, 0, 0, k, &bfull[bs], pol_b);
+                }
+                __syncwarp();
+                if (++bs == static_cast<uint32_t>(SB)) bs = 0;
+            }
+        }
+        (void)b;
     } else if (warp == C::kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         constexpr uint32_t idesc = umma_idesc_f16(kTileM, NPAD);
