@@ -520,9 +520,12 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
 // zero-filled by TMA (weights and activations), contributing exact zeros.
 //
 // Warps: 0 .. 4G-1 de-quantisers (group w/4, TMEM lane quarter w%4),
-// 4G .. 4G+3 epilogue (quarter w%4), 4G+4 MMA issuer, 4G+5 weight producer
-// (also allocates TMEM), 4G+6 activation producer.
-template <int F, int NPAD, int KS_, int G_, int P_ = 2>
+// 4G .. 4G+3 epilogue (quarter w%4), 4G+4 MMA issuer, 4G+5 .. 4G+4+P weight
+// producers (the first also allocates TMEM), 4G+5+P activation producer.
+#ifndef FPX_DEC_PW
+#define FPX_DEC_PW 1
+#endif
+template <int F, int NPAD, int KS_, int G_, int P_ = FPX_DEC_PW>
 struct GCfg {
     static constexpr int kKS = KS_;
     static constexpr int kG = G_;
@@ -530,7 +533,8 @@ struct GCfg {
     static constexpr int kEpiWarp0 = 4 * kG;
     static constexpr int kMmaWarp = kEpiWarp0 + 4;
     static constexpr int kProdWarp = kMmaWarp + 1;
-    static constexpr int kWarps = kProdWarp + kP;
+    static constexpr int kActWarp = kProdWarp + kP;  // kP weight producers, then the activation producer
+    static constexpr int kWarps = kActWarp + 1;
     static constexpr int kThreads = 32 * kWarps;
     static constexpr int kHiBytes = 512 * FmtTraits<F>::kBitsHi;  // per 64x64 tile
     static constexpr int kLoBytes = 512 * FmtTraits<F>::kBitsLo;
@@ -549,10 +553,13 @@ struct GCfg {
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
     static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 4 : 3);
-    // Each ring has exactly one producer warp, which only ever waits on the
-    // consumption of its own previous use of a slot (no parity aliasing).
+    // Weight producer i issues stages i, i+P, ... into slots it alone owns
+    // (SW % P == 0), so it only ever waits on the consumption of its own
+    // previous use of a slot: no parity aliasing.  Several producers because
+    // one warp issues a TMA only every ~0.1 us (measured), below the rate the
+    // HBM roofline needs in bursts.
     static constexpr int kWStages =
-        std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes);
+        std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes) / kP * kP;
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
     static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
 #ifndef FPX_DEC_BS
@@ -565,7 +572,7 @@ struct GCfg {
     static constexpr uint32_t kWTx = 2 * kKS * (kHiBytes + kLoBytes);
     static constexpr uint32_t kBTx = kKS * kBBytes;
     static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
-    static_assert(kP == 2, "one weight producer warp and one activation producer warp");
+    static_assert(kWStages % kP == 0, "each weight slot is owned by one producer warp");
     static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
 
@@ -696,9 +703,9 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
 
     if (p.dbg & 256u) {
         // FPX_LINEAR_DBG=256: launch + prologue + teardown only (bring-up)
-    } else if (warp == C::kProdWarp) {
-        // ------------------------------------------------ weight producer
-        // Weights only, every stage: its sole throttle is the weight ring
+    } else if (warp >= C::kProdWarp && warp < C::kActWarp) {
+        // ------------------------------------------------ weight producers
+        // Weights only, producer pw every P-th stage: the sole throttle is the weight ring
         // (slots come back as soon as a group has the words in registers),
         // so up to SW stages of HBM reads stay in flight.  Sharing a warp with
         // the activation loads -- whose slots come back only with MMA
@@ -706,14 +713,16 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         // ring's.  Weights are immutable during the call, so under PDL they
         // are requested BEFORE waiting for the preceding kernel.
         const bool leader = lane == 0;
+        const uint32_t pw = warp - C::kProdWarp;
         const uint64_t pol_w = policy_evict_first();
         const uint32_t wtx = (p.dbg & 4u) ? 0u : C::kWTx;
-        uint32_t si = 0, ws = 0, wph = 0;  // stage, weight slot, slot parity
+        uint32_t si = 0, ws = pw, wph = 0;  // stage, weight slot, slot parity
         for (uint32_t u = u_begin; u < u_end; ++u) {
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
             const int32_t tr0 = static_cast<int32_t>(2 * mt);
             for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
+                if (si % C::kP != pw) continue;
                 const int32_t k = static_cast<int32_t>((s0 + ls) * KS);
                 // slot free once the group that read it (stage si - SW) released it
                 if (si >= static_cast<uint32_t>(SW)) wait_rec(p, &wempty[ws], wph ^ 1u, 1, si);
@@ -727,10 +736,11 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     }
                 }
                 __syncwarp();
-                if (++ws == static_cast<uint32_t>(SW)) ws = 0, wph ^= 1u;
+                ws += C::kP;
+                if (ws >= static_cast<uint32_t>(SW)) ws -= SW, wph ^= 1u;
             }
         }
-    } else if (warp == C::kProdWarp + 1) {
+    } else if (warp == C::kActWarp) {
         // ------------------------------------------------ activation producer
         // Activations may be written by the preceding kernel: wait for it.
         grid_dep_wait();
