@@ -955,9 +955,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         for (uint32_t u = u_begin; u < u_end; ++u) {
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
-            const uint32_t tr = 2 * mt + r;
-            const bool valid = tr < p.tile_rows;
-            uint32_t sc[2][2];
+            uint32_t sc[2][2];  // zero for a missing tile-row (fetch_scales)
 #pragma unroll
             for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
@@ -982,16 +980,12 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 if (lane == 0) mbar_arrive(&wempty[ws]);
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
-                    // Rows of a missing second tile-row (odd tile_rows) and the
-                    // FPX_LINEAR_DBG=1 no-math mode store zeros: every A-slot lane
-                    // an MMA reads has been written by this CTA.
+                    // A missing second tile-row (odd tile_rows) arrives zero-filled
+                    // by TMA and is multiplied by a zero scale: every A-slot lane
+                    // an MMA reads holds an exact zero.  (No separate zeroing
+                    // path: ptxas if-converted it into every stage.)
                     uint32_t o0[16], o1[16];
-                    if (valid && !(p.dbg & 1u)) {
-                        dequant_words<F>(w[kk], h, sc, o0, o1);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) o0[i] = 0u, o1[i] = 0u;
-                    }
+                    dequant_words<F>(w[kk], h, sc, o0, o1);
                     if (kk == 0) {
                         // A slot `as` last held stage si - R: free once that stage's batch completed
                         if (q == 0 && lane == 0) trace_mark(p, kTrDqDone, si);
