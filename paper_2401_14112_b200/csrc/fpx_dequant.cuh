@@ -187,11 +187,16 @@ FPX_DEV void swar_to_half2(uint32_t x, uint32_t& r1, uint32_t& r2) {
     }
 }
 
-// One slice of one half-warp-tile: 4 iterations -> {R1, R2} per j, already
-// multiplied (fp16 RNE) by the row scales.  sc[lc][0] = scale (both halves)
+// One slice of one half-warp-tile: 4 iterations -> {R1, R2} per j, by
+// default multiplied (fp16 RNE) by the row scales.  sc[lc][0] = scale (both halves)
 // of row 16(2h+lc)+t/4, sc[lc][1] of +8: RAW scales for kHwCvt, effective
 // scales for kSwar (see row_scale_for).
-template <int F, int P = kHwCvt>
+//
+// kScale = false (kHwCvt only): skip the multiply and return fp16(decode)
+// exactly; the caller applies the row scale later in fp32 (the linear
+// kernel's epilogue, for rows whose scales make fp16(decode * s) a normal,
+// finite number -- see fpx_linear.cu).
+template <int F, int P = kHwCvt, bool kScale = true>
 FPX_DEV void dequant_slice_half(uint32_t wa, uint32_t wb, uint32_t wc, int h, const uint32_t (&sc)[2][2],
                                 uint32_t (&r1)[4], uint32_t (&r2)[4]) {
     if constexpr (P == kHwCvt) {
@@ -201,8 +206,13 @@ FPX_DEV void dequant_slice_half(uint32_t wa, uint32_t wb, uint32_t wc, int h, co
         for (int j = 0; j < 4; ++j) {
             uint32_t a, b;
             cvt_pairs<F == kE3M2 ? kE3M2 : kE2M3>(c[j], a, b);
-            r1[j] = hmul2_rn(a, sc[j >> 1][0]);
-            r2[j] = hmul2_rn(b, sc[j >> 1][1]);
+            if constexpr (kScale) {
+                r1[j] = hmul2_rn(a, sc[j >> 1][0]);
+                r2[j] = hmul2_rn(b, sc[j >> 1][1]);
+            } else {
+                r1[j] = a;
+                r2[j] = b;
+            }
         }
     } else {
 #pragma unroll

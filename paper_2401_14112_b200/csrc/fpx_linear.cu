@@ -197,13 +197,13 @@ __device__ __forceinline__ void load_ktile_words(uint32_t hi, uint32_t lo, int h
     }
 }
 
-template <int F>
+template <int F, bool kScale = true>
 __device__ __forceinline__ void dequant_words(const uint32_t (&w)[12], int h, const uint32_t (&sc)[2][2],
                                               uint32_t (&o0)[16], uint32_t (&o1)[16]) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         uint32_t r1[4], r2[4];
-        dequant_slice_half<F, kHwCvt>(w[3 * s], w[3 * s + 1], w[3 * s + 2], h, sc, r1, r2);
+        dequant_slice_half<F, kHwCvt, kScale>(w[3 * s], w[3 * s + 1], w[3 * s + 2], h, sc, r1, r2);
         o0[4 * s + 0] = r1[0];
         o0[4 * s + 1] = r2[0];
         o0[4 * s + 2] = r1[1];
@@ -576,6 +576,21 @@ struct GCfg {
     static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
 
+// Scale placement of the decode kernel, per (unit, 32-row TMEM lane quarter):
+// when every row scale s of the quarter lies in [2^-10, 2^11], fp16(decode *
+// s) is a normal finite fp16 for every nonzero code of every format (|decode|
+// in [2^-4, 28]), i.e. the reference's rounded weight differs from decode * s
+// by at most 2^-11 relatively.  Those quarters feed the MMA fp16(decode)
+// exactly and multiply the fp32 accumulator by s in the epilogue -- 8 fewer
+// instructions per 16 weights on the de-quantisers' critical path, and
+// closer to exact arithmetic.  Quarters with any scale outside the range
+// (subnormal products, potential overflow, the missing rows of an odd last
+// tile-row) keep the reference's in-register fp16 multiply bit for bit.
+// Both sides of the split (de-quantiser warp q and epilogue warp q cover the
+// same 32 rows) take the same warp vote over the same scales, and every CTA
+// handling a chunk of the tile agrees, so split-K stays deterministic.
+__device__ __forceinline__ bool scale_in_epilogue_ok(uint16_t raw) { return raw >= 0x1400u && raw <= 0x6800u; }
+
 // Stage-granular unit range: chunk c of a 128-row tile covers stages
 // [c*NST/split, (c+1)*NST/split), NST = ceil(KT/KS).
 template <int KS>
@@ -836,6 +851,11 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             tc_fence_after();
             const uint32_t m = mt * kTileM + row_l;
             const bool row_ok = m < p.rows_p;
+            // the de-quantiser warps of this lane quarter took the same vote
+            // (scale_in_epilogue_ok): if it passed, apply the row scale here
+            const uint16_t raw_s = 2 * mt + (q >> 1) < p.tile_rows ? __ldg(&p.scales[m]) : uint16_t(0);
+            const bool epi_scale = __all_sync(0xffffffffu, scale_in_epilogue_ok(raw_s));
+            const float s_row = epi_scale ? __half2float(__ushort_as_half(raw_s)) : 1.0f;
             // split-K partials: [unit][col/4][row][4] fp32 -- a lane's 4 columns
             // are one 16-byte vector and a warp's 32 rows are contiguous, so the
             // stores here and the loads of the reduction are coalesced float4s
@@ -847,6 +867,10 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 if (ns > 0) {
                     tmem_ld_32x32b_x16(tacc + c0, v);
                     tmem_ld_wait();
+                    if (epi_scale) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * s_row);
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] = 0u;  // empty K chunk contributes zero
@@ -956,57 +980,71 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
             uint32_t sc[2][2];  // zero for a missing tile-row (fetch_scales)
+            bool ok_t = true;
 #pragma unroll
             for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) sc[lc][hf] = row_scale_for<F, kHwCvt>(nxt[lc][hf]);
+                for (int hf = 0; hf < 2; ++hf) {
+                    sc[lc][hf] = row_scale_for<F, kHwCvt>(nxt[lc][hf]);
+                    ok_t = ok_t && scale_in_epilogue_ok(nxt[lc][hf]);
+                }
+            // warp-uniform: the scale goes to the epilogue for this unit's 32 rows
+            const bool epi_scale = __all_sync(0xffffffffu, ok_t);
             if (u + 1 < u_end) fetch_scales(u + 1, nxt);
             // this group's stages of the unit: si % G == g
             uint32_t ls = (g + G - si % G) % G;
-            for (si += ls; ls < ns; ls += G, si += G) {
-                const uint32_t ws = si % SW, as = si % R;
-                const uint32_t wb = smem_u32(wring + ws * C::kWStageBytes);
-                if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
-                wait_rec(p, &wfull[ws], (si / SW) & 1u, 3, si);
-                if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);
-                // all of the stage's packed words into registers, then hand the
-                // weight stage back to the producers
-                uint32_t w[KS][12];
+            // Two copies of the stage loop (scale in registers / in the
+            // epilogue), selected once per unit: a per-stage select was
+            // if-converted by ptxas into executing both.
+            auto stage_loop = [&](auto scale_tag) {
+                constexpr bool kScale = decltype(scale_tag)::value;
+                for (si += ls; ls < ns; ls += G, si += G) {
+                    const uint32_t ws = si % SW, as = si % R;
+                    const uint32_t wb = smem_u32(wring + ws * C::kWStageBytes);
+                    if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
+                    wait_rec(p, &wfull[ws], (si / SW) & 1u, 3, si);
+                    if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);
+                    // all of the stage's packed words into registers, then hand the
+                    // weight stage back to the producers
+                    uint32_t w[KS][12];
 #pragma unroll
-                for (int kk = 0; kk < KS; ++kk)
-                    load_ktile_words<F>(wb + (r * KS + kk) * C::kHiBytes, wb + C::kLoOff + (r * KS + kk) * C::kLoBytes,
-                                        h, lane, w[kk]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&wempty[ws]);
+                    for (int kk = 0; kk < KS; ++kk)
+                        load_ktile_words<F>(wb + (r * KS + kk) * C::kHiBytes, wb + C::kLoOff + (r * KS + kk) * C::kLoBytes,
+                                            h, lane, w[kk]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wempty[ws]);
 #pragma unroll
-                for (int kk = 0; kk < KS; ++kk) {
-                    // A missing second tile-row (odd tile_rows) arrives zero-filled
-                    // by TMA and is multiplied by a zero scale: every A-slot lane
-                    // an MMA reads holds an exact zero.  (No separate zeroing
-                    // path: ptxas if-converted it into every stage.)
-                    uint32_t o0[16], o1[16];
-                    dequant_words<F>(w[kk], h, sc, o0, o1);
-                    if (kk == 0) {
-                        // A slot `as` last held stage si - R: free once that stage's batch completed
-                        if (q == 0 && lane == 0) trace_mark(p, kTrDqDone, si);
-                        if (si >= static_cast<uint32_t>(R)) {
-                            const uint32_t b = (si - R) / BS;
-                            wait_rec(p, &done[b % NB], (b / NB) & 1u, 6, si);
+                    for (int kk = 0; kk < KS; ++kk) {
+                        // A missing second tile-row (odd tile_rows) arrives zero-filled
+                        // by TMA and is multiplied by a zero scale: every A-slot lane
+                        // an MMA reads holds an exact zero.  (No separate zeroing
+                        // path: ptxas if-converted it into every stage.)
+                        uint32_t o0[16], o1[16];
+                        dequant_words<F, kScale>(w[kk], h, sc, o0, o1);
+                        if (kk == 0) {
+                            // A slot `as` last held stage si - R: free once that stage's batch completed
+                            if (q == 0 && lane == 0) trace_mark(p, kTrDqDone, si);
+                            if (si >= static_cast<uint32_t>(R)) {
+                                const uint32_t b = (si - R) / BS;
+                                wait_rec(p, &done[b % NB], (b / NB) & 1u, 6, si);
+                            }
+                            if (q == 0 && lane == 0) trace_mark(p, kTrDqDone1, si);
+                            tc_fence_after();
                         }
-                        if (q == 0 && lane == 0) trace_mark(p, kTrDqDone1, si);
-                        tc_fence_after();
+                        tmem_st_16x128b_x8(tq + (as * KS + kk) * 32, o0);
+                        tmem_st_16x128b_x8(tq + (as * KS + kk) * 32 + (16u << 16), o1);
                     }
-                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32, o0);
-                    tmem_st_16x128b_x8(tq + (as * KS + kk) * 32 + (16u << 16), o1);
+                    tmem_st_wait();
+                    tc_fence_before();
+                    // the MMA reads this stage's activations: make sure they landed
+                    wait_rec(p, &bfull[si % SB], (si / SB) & 1u, 8, si);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aready[as]);
+                    if (q == 0 && lane == 0) trace_mark(p, kTrMmaAfull, si);
                 }
-                tmem_st_wait();
-                tc_fence_before();
-                // the MMA reads this stage's activations: make sure they landed
-                wait_rec(p, &bfull[si % SB], (si / SB) & 1u, 8, si);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&aready[as]);
-                if (q == 0 && lane == 0) trace_mark(p, kTrMmaAfull, si);
-            }
+            };
+            if (epi_scale) stage_loop(std::false_type{});
+            else stage_loop(std::true_type{});
             si -= ls - ns;  // back to the first stage of the next unit
         }
     }
