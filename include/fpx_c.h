@@ -141,7 +141,9 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
                        uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream);
 
 /* ---- debug ------------------------------------------------------------
- * With FPX_LINEAR_TRACE=1 in the environment, every fpx_linear launch records
+ * Only a tracing build records anything (make -C paper_2401_14112_b200 trace
+ * -> libfpx_b200_trace.so); the production library compiles the device-side
+ * stamps out.  With FPX_LINEAR_TRACE=1 in the environment, every fpx_linear launch records
  * clock64 stamps of CTA 0's pipeline events (7 events x 512 stages, row-major)
  * which this call copies to host (synchronous). */
 int fpx_debug_trace(uint64_t* host, size_t words);

@@ -82,23 +82,31 @@ struct KParams {
 
 // Debug (FPX_LINEAR_TRACE=3): record, in mapped host memory the host can read
 // while a launch is stuck, which barrier each warp is waiting on.
+// Device-side tracing (FPX_LINEAR_TRACE=1/2/3 at run time) is compiled in
+// only with -DFPX_TRACE=1 (the bring-up tools load such a build through
+// FPX_B200_LIB): its null checks cost issue slots on the latency-bound
+// de-quantiser path of the production kernel.
+#ifndef FPX_TRACE
+#define FPX_TRACE 0
+#endif
 __device__ __forceinline__ void wait_rec(const KParams& p, uint64_t* bar, uint32_t parity, uint32_t tag,
                                          uint32_t si) {
-    if (p.prog != nullptr) {
+    if (FPX_TRACE && p.prog != nullptr) {
         const uint32_t w = threadIdx.x >> 5;
         p.prog[blockIdx.x * 32 + w] = (1ull << 63) | (static_cast<unsigned long long>(tag) << 56) |
                                       (static_cast<unsigned long long>(si & 0xffffffu) << 32) |
                                       (static_cast<unsigned long long>(smem_u32(bar)) << 1) | parity;
     }
     mbar_wait(bar, parity);
-    if (p.prog != nullptr) p.prog[blockIdx.x * 32 + (threadIdx.x >> 5)] = 0;
+    if (FPX_TRACE && p.prog != nullptr) p.prog[blockIdx.x * 32 + (threadIdx.x >> 5)] = 0;
 }
 
 // trace slots: [event][stage], kTraceStages stages per event
 constexpr int kTraceStages = 512;
 enum TraceEv { kTrProdIssue = 0, kTrDqAempty, kTrDqFull, kTrDqDone, kTrMmaAfull, kTrMmaIssued, kTrEpiFull, kTrDqDone1, kTrDqDone2, kTrDqDone3, kTrMmaWait, kTrMmaGo, kTrNumEv };
 __device__ __forceinline__ void trace_mark(const KParams& p, int ev, uint32_t si) {
-    if (p.trace != nullptr && blockIdx.x == 0 && si < kTraceStages) p.trace[ev * kTraceStages + si] = clock64();
+    if (FPX_TRACE && p.trace != nullptr && blockIdx.x == 0 && si < kTraceStages)
+        p.trace[ev * kTraceStages + si] = clock64();
 }
 
 // Whole-grid timeline (globaltimer ns): per CTA slot e (0 = start after the
@@ -107,7 +115,7 @@ __device__ __forceinline__ void trace_mark(const KParams& p, int ev, uint32_t si
 // done, 12 = teardown (all warps done), 13 = TMEM freed), at
 // trace[12*512 + cta*16 + e].
 __device__ __forceinline__ void trace_cta(const KParams& p, uint32_t e) {
-    if (p.trace != nullptr && blockIdx.x < 256 && e < 16) {
+    if (FPX_TRACE && p.trace != nullptr && blockIdx.x < 256 && e < 16) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[12 * kTraceStages + blockIdx.x * 16 + e] = t;

@@ -12,6 +12,7 @@ import numpy as np
 os.environ["FPX_LINEAR_TRACE"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("FPX_B200_LIB", os.path.join(ROOT, "paper_2401_14112_b200", "libfpx_b200_trace.so"))  # make ... trace
 import torch  # noqa: E402
 
 import paper_2401_14112_b200 as fpx  # noqa: E402
