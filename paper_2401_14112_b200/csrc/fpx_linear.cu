@@ -735,6 +735,10 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         // completion -- capped the weight prefetch depth at the activation
         // ring's.  Weights are immutable during the call, so under PDL they
         // are requested BEFORE waiting for the preceding kernel.
+        // PDL mode 2 (default): packed weights are immutable while linears run
+        // (inference), so the weight stream starts before the preceding kernel
+        // has finished; mode 1 waits for it like every other global read.
+        if (p.pdl != 2u) grid_dep_wait();
         const bool leader = lane == 0;
         const uint32_t pw = warp - C::kProdWarp;
         const uint64_t pol_w = policy_evict_first();
@@ -981,6 +985,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     raw[lc][hf] = tr_ < p.tile_rows ? __ldg(&p.scales[tr_ * 64 + 16 * (2 * h + lc) + 8 * hf + lane / 4])
                                                     : uint16_t(0);
         };
+        if (p.pdl != 2u) grid_dep_wait();  // row scales: immutable like the weights in mode 2
         uint16_t nxt[2][2] = {{0, 0}, {0, 0}};
         if (u_begin < u_end) fetch_scales(u_begin, nxt);
         uint32_t si = 0;
@@ -1086,18 +1091,23 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Launch with programmatic stream serialization (PDL) when FPX_LINEAR_PDL=1:
-// the kernel may start (prologue, weight prefetch) while the preceding
-// kernel in the stream drains; its griddepcontrol.wait orders everything
-// that depends on that kernel.  Off by default: worth ~2 us per launch, but
-// back-to-back PDL launches were seen to fault / hang in a debug mode
-// (FPX_LINEAR_DBG=1) that is not yet understood.
-static bool pdl_enabled() {
-    static const bool on = [] {
+// Programmatic dependent launch (FPX_LINEAR_PDL, read once):
+//   2 (default) the kernel may start while the preceding kernel in the stream
+//     drains: prologue, TMEM allocation and the weight / row-scale stream
+//     begin at once; activations, C, partials and counters are touched only
+//     after griddepcontrol.wait.  Requires that packed weights and scales are
+//     not written by a preceding kernel that triggers dependents early
+//     (inference: weights are static).  Measured ~3.5 us per launch.
+//   1 PDL with every global access after griddepcontrol.wait (hides the
+//     launch latency and prologue only, ~1.2 us).
+//   0 plain stream order.
+static uint32_t pdl_mode() {
+    static const uint32_t mode = [] {
         const char* e = std::getenv("FPX_LINEAR_PDL");
-        return e != nullptr && std::atoi(e) != 0;
+        const int v = e != nullptr ? std::atoi(e) : 2;
+        return static_cast<uint32_t>(v < 0 ? 0 : (v > 2 ? 2 : v));
     }();
-    return on;
+    return mode;
 }
 
 template <typename Kern, typename... Args>
@@ -1111,7 +1121,7 @@ cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = pdl_mode() != 0 ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -1201,7 +1211,7 @@ cudaError_t launch_g(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    kq.pdl = pdl_enabled() ? 1u : 0u;
+    kq.pdl = pdl_mode();
     return launch_pdl(kern, grid, C::kThreads, C::kSmemBytes, st, map, hi_map, lo_map, kq);
 }
 
