@@ -1285,9 +1285,15 @@ int linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n, int num_s
     double best = 1e30;
     int best_s = 1;
     const int smax = static_cast<int>(std::min<uint32_t>(kt, 64));
+    // Waves x (k-tiles per unit + per-unit overhead).  The overhead, ~10
+    // k-tiles (pipeline drain/refill around the accumulator hand-off and the
+    // epilogue), was fitted on B200 to the measured best splits of SURVEY
+    // §8d's shapes (bench_configs.py --sweep-splits: 8192x22016, 22016x8192,
+    // the five 70B linears, 4096^2); it makes fewer, longer units win over
+    // finer load balance.  Split-K partial traffic adds a little per unit.
     for (int s = 1; s <= smax; ++s) {
         const double per_cta = std::ceil(double(tiles_m) * s / num_sms);
-        const double pen = 1.0 + (s > 1 ? 0.25 * (2.0 * kTileM * n * 4.0) / 6144.0 : 0.0);
+        const double pen = 10.0 + (s > 1 ? 0.25 * (2.0 * kTileM * n * 4.0) / 6144.0 : 0.0);
         const double est = per_cta * (std::ceil(double(kt) / s) + pen);
         if (est < best - 1e-9) best = est, best_s = s;
     }
