@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <filesystem>
 #include <vector>
 
 namespace fpx {
@@ -165,6 +166,19 @@ QuantizedMatrix unpack(const PackedWeights& p);
 ScalarMatrix dequantize(const PackedWeights& p);
 // C fp32 col-major (padded rows x n) = dequant(A) x B, B fp16 col-major.
 ScalarMatrix gemm_packed(const PackedWeights& a, const ScalarMatrix& b, BankAccessTrace* trace = nullptr);
+
+// io.hpp:27-41 -- MatrixFile ("FPXMAT1\0") and PackFile ("FPXPACK1")
+// containers, little-endian, strict validation (Truncated / BadMagic /
+// BadVersion / Corrupt errors carry the byte offset).
+std::vector<uint8_t> serialize_matrix(const ScalarMatrix& m);
+ScalarMatrix deserialize_matrix(const std::vector<uint8_t>& bytes);
+std::vector<uint8_t> serialize_packed(const PackedWeights& p);
+PackedWeights deserialize_packed(const std::vector<uint8_t>& bytes);
+void write_matrix_file(const std::filesystem::path& path, const ScalarMatrix& m);
+ScalarMatrix read_matrix_file(const std::filesystem::path& path);
+void write_pack_file(const std::filesystem::path& path, const PackedWeights& p);
+PackedWeights read_pack_file(const std::filesystem::path& path);
+ScalarMatrix read_raw_blob(const std::filesystem::path& path, Dtype dtype, uint32_t rows, uint32_t cols);
 
 // Weights resident in HBM for repeated linears (the inference use).
 class DeviceLinear {

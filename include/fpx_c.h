@@ -71,6 +71,9 @@ enum fpx_dtype { FPX_FP32 = 0, FPX_FP16 = 1 }; /* codec.hpp:10 Dtype */
 
 /* ---- library / host-only helpers (no GPU needed) ---------------------- */
 const char* fpx_last_error(void);
+/* Byte offset carried by the last error on this thread (file errors,
+ * error.hpp:35-41 Error::offset), or -1. */
+int64_t fpx_last_error_offset(void);
 const char* fpx_status_name(int status);   /* error.cpp:5-22 names */
 int fpx_version(void);                     /* major*10000 + minor*100 + patch */
 int fpx_format_check(int exp_bits, int man_bits);            /* 0 or FPX_ERR_INVALID_FORMAT */
@@ -147,6 +150,39 @@ void fpx_shard_rows(uint32_t rows_p, int rank, int world, uint32_t* tr0, uint32_
  * of per-rank first row / row count.  Writes col-major c (ldc). */
 int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32_t* nrows, int world,
                        uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream);
+
+/* ---- PackFile container (io.hpp:13-41, SPEC.md model-io; host only) ----
+ * "FPXPACK1" | u16 version=1 | u8 exp_bits | u8 man_bits | u8 nseg |
+ * u8 widths[nseg] (high bits first) | u32 orig_rows, orig_cols, padded_rows,
+ * padded_cols, tile_m=64, tile_k=64 | u8 scale granularity=0 |
+ * u16 scales[padded_rows] | per segment: u64 length + stream bytes.
+ * Little-endian throughout.  The reference declares this container
+ * (io.hpp:36-37 write_pack_file / read_pack_file) but never implements it.
+ * Errors: FPX_ERR_BAD_MAGIC, _BAD_VERSION, _TRUNCATED, _CORRUPT (length /
+ * size-law / dimension violations, trailing bytes), _UNSUPPORTED_SPLIT,
+ * _INVALID_FORMAT, _IO_FAILURE; fpx_last_error_offset() names the byte. */
+typedef struct fpx_pack_header {
+    int exp_bits, man_bits, nseg;
+    int widths[3];
+    uint32_t orig_rows, orig_cols, rows_p, cols_p;
+    uint64_t scales_offset;     /* file offset of scales[0] */
+    uint64_t stream_offset[3];  /* file offset of each stream's first byte */
+    uint64_t stream_bytes[3];
+    uint64_t file_bytes;
+} fpx_pack_header;
+size_t fpx_packfile_bytes(uint32_t rows_p, uint32_t cols_p, const int* widths, int nseg);
+/* Serialise host buffers into out[0 .. fpx_packfile_bytes()). */
+int fpx_packfile_encode(int exp_bits, int man_bits, const int* widths, int nseg, uint32_t orig_rows,
+                        uint32_t orig_cols, uint32_t rows_p, uint32_t cols_p, const uint16_t* scales,
+                        const uint8_t* const* streams, uint8_t* out, size_t out_bytes);
+/* Validate a complete in-memory file and describe it. */
+int fpx_packfile_parse(const uint8_t* bytes, size_t nbytes, fpx_pack_header* hdr);
+/* Validate the file at `path` (header, size law, stream lengths, total size)
+ * and, unless scales_dev is NULL (header only), copy its scales and streams
+ * straight into the caller's device buffers on `stream` through pinned
+ * staging (synchronous on return). */
+int fpx_packfile_load(const char* path, fpx_pack_header* hdr, uint16_t* scales_dev, uint8_t* const* streams_dev,
+                      fpx_stream_t stream);
 
 /* ---- debug ------------------------------------------------------------
  * Only a tracing build records anything (make -C paper_2401_14112_b200 trace

@@ -23,6 +23,14 @@ _intp = C.POINTER(C.c_int)
 _lib = None
 
 
+class PackHeader(C.Structure):
+    """fpx_pack_header (include/fpx_c.h)."""
+    _fields_ = [("exp_bits", C.c_int), ("man_bits", C.c_int), ("nseg", C.c_int), ("widths", C.c_int * 3),
+                ("orig_rows", C.c_uint32), ("orig_cols", C.c_uint32), ("rows_p", C.c_uint32), ("cols_p", C.c_uint32),
+                ("scales_offset", C.c_uint64), ("stream_offset", C.c_uint64 * 3), ("stream_bytes", C.c_uint64 * 3),
+                ("file_bytes", C.c_uint64)]
+
+
 def header_symbols() -> list[str]:
     """Every function the public header declares (parsed from include/fpx_c.h)."""
     text = open(HEADER).read()
@@ -63,6 +71,13 @@ def load(path: str | None = None) -> C.CDLL:
         "fpx_linear": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int,
                                  C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
+        "fpx_last_error_offset": (C.c_int64, []),
+        "fpx_packfile_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, _intp, C.c_int]),
+        "fpx_packfile_encode": (C.c_int, [C.c_int, C.c_int, _intp, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.c_size_t]),
+        "fpx_packfile_parse": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(PackHeader)]),
+        "fpx_packfile_load": (C.c_int, [C.c_char_p, C.POINTER(PackHeader), C.c_void_p, C.POINTER(C.c_void_p),
+                                        C.c_void_p]),
         "fpx_debug_trace": (C.c_int, [C.c_void_p, C.c_size_t]),
         "fpx_debug_progress": (C.c_void_p, []),
         "fpx_shard_rows": (None, [C.c_uint32, C.c_int, C.c_int, _u32p, _u32p]),

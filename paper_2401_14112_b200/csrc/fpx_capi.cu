@@ -14,11 +14,13 @@
 #include <string>
 
 #include "../../include/fpx_c.h"
+#include "fpx_internal.h"
 #include "fpx_kernels.h"
 
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int64_t g_last_offset = -1;
 
 const char* kNames[] = {"ok",            "invalid-format", "invalid-code",       "invalid-value",
                         "scale-overflow", "shape-mismatch", "ragged-input",       "unsupported-split",
@@ -32,6 +34,7 @@ int fail(int status, const char* fmt, ...) {
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
     g_last_error = std::string("error[") + fpx_status_name(status) + "] " + buf;
+    g_last_offset = -1;
     return status;
 }
 
@@ -143,6 +146,7 @@ volatile unsigned long long* debug_progress_buffer() {
 extern "C" {
 
 const char* fpx_last_error(void) { return g_last_error.c_str(); }
+int64_t fpx_last_error_offset(void) { return g_last_offset; }
 
 const char* fpx_status_name(int s) {
     if (s >= 0 && s <= 13) return kNames[s];
@@ -436,3 +440,12 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
 }
 
 }  // extern "C"
+
+namespace fpxi {
+int set_error(int status, const std::string& msg, int64_t offset) {
+    g_last_error = std::string("error[") + fpx_status_name(status) + "] " + msg;
+    if (offset >= 0) g_last_error += " (at byte " + std::to_string(offset) + ")";
+    g_last_offset = offset;
+    return status;
+}
+}  // namespace fpxi

@@ -7,6 +7,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <string>
 
 #include "fpx_b200.hpp"
@@ -22,6 +24,13 @@ namespace {
     if (msg.rfind("error[", 0) == 0) {
         const size_t close = msg.find("] ");
         if (close != std::string::npos) msg = msg.substr(close + 2);
+    }
+    const int64_t off = fpx_last_error_offset();
+    if (off >= 0) {
+        const std::string suffix = " (at byte " + std::to_string(off) + ")";
+        if (msg.size() >= suffix.size() && msg.compare(msg.size() - suffix.size(), suffix.size(), suffix) == 0)
+            msg.resize(msg.size() - suffix.size());
+        if (st >= 1 && st <= 13) throw Error(static_cast<ErrorCode>(st - 1), msg, static_cast<uint64_t>(off));
     }
     if (st >= 1 && st <= 13) throw Error(static_cast<ErrorCode>(st - 1), msg);
     throw DeviceError(std::string("error[") + fpx_status_name(st) + "] " + msg);
@@ -342,6 +351,128 @@ ScalarMatrix gemm_packed(const PackedWeights& a, const ScalarMatrix& b, BankAcce
     check_problem(a.cols, a.orig_cols, b);
     DeviceLinear lin(a);
     return lin.forward(b);
+}
+
+// ------------------------------------------------------------------ io.hpp
+// PackFile over the C-ABI container code (fpx_io.cpp); MatrixFile here.
+// Both little-endian with strict validation (SPEC.md model-io).
+namespace {
+constexpr char kMatMagic[8] = {'F', 'P', 'X', 'M', 'A', 'T', '1', 0};
+
+template <typename T>
+void put(std::vector<uint8_t>& o, T v) {
+    for (size_t i = 0; i < sizeof(T); ++i) o.push_back(static_cast<uint8_t>(static_cast<uint64_t>(v) >> (8 * i)));
+}
+template <typename T>
+T get(const std::vector<uint8_t>& b, size_t& off, const char* what) {
+    if (b.size() < off || b.size() - off < sizeof(T))
+        throw Error(ErrorCode::Truncated, std::string("matrix file ends inside ") + what, off);
+    uint64_t x = 0;
+    for (size_t i = 0; i < sizeof(T); ++i) x |= static_cast<uint64_t>(b[off + i]) << (8 * i);
+    off += sizeof(T);
+    return static_cast<T>(x);
+}
+std::vector<uint8_t> read_all(const std::filesystem::path& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw Error(ErrorCode::IoFailure, "cannot open " + path.string());
+    return std::vector<uint8_t>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+void write_all(const std::filesystem::path& path, const std::vector<uint8_t>& b) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f || !f.write(reinterpret_cast<const char*>(b.data()), static_cast<std::streamsize>(b.size())))
+        throw Error(ErrorCode::IoFailure, "cannot write " + path.string());
+}
+}  // namespace
+
+std::vector<uint8_t> serialize_matrix(const ScalarMatrix& m) {
+    std::vector<uint8_t> o(kMatMagic, kMatMagic + 8);
+    put<uint32_t>(o, static_cast<uint32_t>(m.dtype));
+    put<uint32_t>(o, m.rows);
+    put<uint32_t>(o, m.cols);
+    put<uint8_t>(o, static_cast<uint8_t>(m.layout));
+    for (int i = 0; i < 3; ++i) put<uint8_t>(o, 0);
+    if (m.dtype == Dtype::Fp32)
+        for (float v : m.f32) {
+            uint32_t u;
+            std::memcpy(&u, &v, 4);
+            put<uint32_t>(o, u);
+        }
+    else
+        for (uint16_t v : m.f16) put<uint16_t>(o, v);
+    return o;
+}
+
+ScalarMatrix deserialize_matrix(const std::vector<uint8_t>& b) {
+    if (b.size() < 8) throw Error(ErrorCode::Truncated, "matrix file ends inside the magic", 0);
+    if (std::memcmp(b.data(), kMatMagic, 8) != 0) throw Error(ErrorCode::BadMagic, "not an FPXMAT1 file", 0);
+    size_t off = 8;
+    const uint32_t dt = get<uint32_t>(b, off, "the dtype");
+    if (dt > 1) throw Error(ErrorCode::Corrupt, "dtype " + std::to_string(dt), 8);
+    const uint32_t rows = get<uint32_t>(b, off, "the dimensions"), cols = get<uint32_t>(b, off, "the dimensions");
+    const uint8_t lo = get<uint8_t>(b, off, "the layout");
+    if (lo > 1) throw Error(ErrorCode::Corrupt, "layout " + std::to_string(lo), off - 1);
+    off += 3;
+    const size_t es = dt == 0 ? 4 : 2, n = size_t(rows) * cols;
+    if (b.size() < off || b.size() - off < n * es)
+        throw Error(ErrorCode::Truncated, "matrix file ends inside the payload", b.size());
+    if (b.size() - off != n * es) throw Error(ErrorCode::Corrupt, "trailing bytes after the payload", off + n * es);
+    ScalarMatrix m = ScalarMatrix::zeros(static_cast<Dtype>(dt), static_cast<Layout>(lo), rows, cols);
+    if (dt == 0)
+        std::memcpy(m.f32.data(), b.data() + off, n * 4);  // little-endian host (x86-64 / aarch64)
+    else
+        std::memcpy(m.f16.data(), b.data() + off, n * 2);
+    return m;
+}
+
+std::vector<uint8_t> serialize_packed(const PackedWeights& p) {
+    const int nseg = static_cast<int>(p.split.widths.size());
+    std::vector<const uint8_t*> sp;
+    for (const auto& s : p.streams) sp.push_back(s.data());
+    std::vector<uint8_t> out(fpx_packfile_bytes(p.rows, p.cols, p.split.widths.data(), nseg));
+    for (int i = 0; i < nseg; ++i)
+        if (i >= static_cast<int>(p.streams.size()) ||
+            p.streams[i].size() != fpx_stream_bytes(p.rows, p.cols, p.split.widths[i]))
+            throw Error(ErrorCode::ShapeMismatch, "stream " + std::to_string(i) + " does not match the size law");
+    if (p.scales.size() != p.rows) throw Error(ErrorCode::ShapeMismatch, "one scale per padded row");
+    check(fpx_packfile_encode(p.format.exp_bits, p.format.man_bits, p.split.widths.data(), nseg, p.orig_rows,
+                              p.orig_cols, p.rows, p.cols, p.scales.data(), sp.data(), out.data(), out.size()));
+    return out;
+}
+
+PackedWeights deserialize_packed(const std::vector<uint8_t>& b) {
+    fpx_pack_header h;
+    check(fpx_packfile_parse(b.data(), b.size(), &h));
+    PackedWeights p;
+    p.format = FpxFormat::make(h.exp_bits, h.man_bits);
+    p.split = SplitScheme::make(std::vector<int>(h.widths, h.widths + h.nseg), p.format);
+    p.rows = h.rows_p;
+    p.cols = h.cols_p;
+    p.orig_rows = h.orig_rows;
+    p.orig_cols = h.orig_cols;
+    p.scales.resize(h.rows_p);
+    std::memcpy(p.scales.data(), b.data() + h.scales_offset, size_t(h.rows_p) * 2);
+    for (int i = 0; i < h.nseg; ++i)
+        p.streams.emplace_back(b.begin() + static_cast<std::ptrdiff_t>(h.stream_offset[i]),
+                               b.begin() + static_cast<std::ptrdiff_t>(h.stream_offset[i] + h.stream_bytes[i]));
+    return p;
+}
+
+void write_matrix_file(const std::filesystem::path& path, const ScalarMatrix& m) { write_all(path, serialize_matrix(m)); }
+ScalarMatrix read_matrix_file(const std::filesystem::path& path) { return deserialize_matrix(read_all(path)); }
+void write_pack_file(const std::filesystem::path& path, const PackedWeights& p) { write_all(path, serialize_packed(p)); }
+PackedWeights read_pack_file(const std::filesystem::path& path) { return deserialize_packed(read_all(path)); }
+
+ScalarMatrix read_raw_blob(const std::filesystem::path& path, Dtype dtype, uint32_t rows, uint32_t cols) {
+    const std::vector<uint8_t> b = read_all(path);
+    const size_t es = dtype == Dtype::Fp32 ? 4 : 2, n = size_t(rows) * cols;
+    if (b.size() != n * es)
+        throw Error(b.size() < n * es ? ErrorCode::Truncated : ErrorCode::Corrupt,
+                    "raw blob holds " + std::to_string(b.size()) + " bytes, expected " + std::to_string(n * es),
+                    std::min(b.size(), n * es));
+    ScalarMatrix m = ScalarMatrix::zeros(dtype, Layout::RowMajor, rows, cols);
+    if (dtype == Dtype::Fp32) std::memcpy(m.f32.data(), b.data(), n * 4);
+    else std::memcpy(m.f16.data(), b.data(), n * 2);
+    return m;
 }
 
 }  // namespace fpx

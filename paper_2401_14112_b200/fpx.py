@@ -35,7 +35,8 @@ from . import _lib
 __all__ = [
     "ErrorCode", "FpxError", "FpxFormat", "SplitScheme", "QuantizedMatrix", "PackedWeights",
     "quantize_matrix", "pack", "unpack", "dequantize", "gemm_packed", "fp6_linear", "effective_scale",
-    "linear_workspace", "default_split",
+    "linear_workspace", "default_split", "serialize_packed", "deserialize_packed", "write_pack_file",
+    "read_pack_file",
 ]
 
 
@@ -72,7 +73,8 @@ class FpxError(RuntimeError):
 def _check(status: int) -> None:
     if status != 0:
         L = _lib.load()
-        raise FpxError(status, L.fpx_last_error().decode())
+        off = int(L.fpx_last_error_offset())
+        raise FpxError(status, L.fpx_last_error().decode(), off if off >= 0 else None)
 
 
 @dataclass(frozen=True)
@@ -327,6 +329,76 @@ def gemm_packed(p: PackedWeights, b: torch.Tensor, *, out: torch.Tensor | None =
                         p.format.man_bits, b.data_ptr(), k_act, n, out.data_ptr(), ldc, sk,
                         _ptr(ws), 0 if ws is None else ws.numel(), _stream(dev)))
     return out
+
+
+# ------------------------------------------------------------ PackFile I/O
+# io.hpp:30-37 (serialize_packed / deserialize_packed / write_pack_file /
+# read_pack_file), the FPXPACK1 container of include/fpx_c.h.
+
+def serialize_packed(p: PackedWeights) -> bytes:
+    """io.hpp:30: PackedWeights -> FPXPACK1 bytes (little-endian, bit-exact)."""
+    import numpy as np
+    L = _lib.load()
+    wid = (C.c_int * len(p.split.widths))(*p.split.widths)
+    host = [s.detach().contiguous().cpu().numpy() for s in p.streams]
+    scales = p.scales.detach().contiguous().cpu().numpy().view(np.uint16)
+    n = int(L.fpx_packfile_bytes(p.rows, p.cols, wid, len(p.split.widths)))
+    out = np.empty(n, dtype=np.uint8)
+    ptrs = (C.c_void_p * len(host))(*[h.ctypes.data for h in host])
+    _check(L.fpx_packfile_encode(p.format.exp_bits, p.format.man_bits, wid, len(p.split.widths), p.orig_rows,
+                                 p.orig_cols, p.rows, p.cols, scales.ctypes.data, ptrs, out.ctypes.data, n))
+    return out.tobytes()
+
+
+def _from_header(h, scales: torch.Tensor, streams: list) -> PackedWeights:
+    fmt = FpxFormat(h.exp_bits, h.man_bits)
+    split = SplitScheme(tuple(h.widths[i] for i in range(h.nseg)))
+    return PackedWeights(fmt, split, h.rows_p, h.cols_p, h.orig_rows, h.orig_cols, streams, scales)
+
+
+def deserialize_packed(data: bytes, device: str | torch.device = "cpu") -> PackedWeights:
+    """io.hpp:31: strict validation (FpxError BadMagic / BadVersion /
+    Truncated / Corrupt with the byte offset), then the tensors on `device`."""
+    import numpy as np
+    L = _lib.load()
+    buf = np.frombuffer(data, dtype=np.uint8)
+    h = _lib.PackHeader()
+    _check(L.fpx_packfile_parse(buf.ctypes.data if buf.size else None, buf.size, C.byref(h)))
+    sc = torch.from_numpy(buf[h.scales_offset: h.scales_offset + 2 * h.rows_p].copy().view(np.int16))
+    streams = [torch.from_numpy(buf[h.stream_offset[i]: h.stream_offset[i] + h.stream_bytes[i]].copy())
+               for i in range(h.nseg)]
+    return _from_header(h, sc.to(device), [t.to(device) for t in streams])
+
+
+def write_pack_file(path: str, p: PackedWeights) -> None:
+    """io.hpp:36."""
+    data = serialize_packed(p)
+    try:
+        with open(path, "wb") as f:
+            f.write(data)
+    except OSError as e:
+        raise FpxError(13, f"error[io-failure] cannot write {path}: {e}")
+
+
+def read_pack_file(path: str, device: str | torch.device = "cuda") -> PackedWeights:
+    """io.hpp:37.  On a CUDA device the payload goes straight from disk into
+    device buffers (fpx_packfile_load: pinned staging, no pageable copy)."""
+    L = _lib.load()
+    dev = torch.device(device)
+    h = _lib.PackHeader()
+    if dev.type != "cuda":
+        try:
+            with open(path, "rb") as f:
+                data = f.read()
+        except OSError as e:
+            raise FpxError(13, f"error[io-failure] cannot open {path}: {e}")
+        return deserialize_packed(data, dev)
+    _check(L.fpx_packfile_load(path.encode(), C.byref(h), None, None, None))  # validate, sizes
+    scales = torch.empty(h.rows_p, dtype=torch.int16, device=dev)
+    streams = [torch.empty(h.stream_bytes[i], dtype=torch.uint8, device=dev) for i in range(h.nseg)]
+    ptrs = (C.c_void_p * h.nseg)(*[t.data_ptr() for t in streams])
+    _check(L.fpx_packfile_load(path.encode(), C.byref(h), scales.data_ptr(), ptrs, _stream(dev)))
+    return _from_header(h, scales, streams)
 
 
 def fp6_linear(act: torch.Tensor, packed: PackedWeights, **kw) -> torch.Tensor:

@@ -323,3 +323,56 @@ def test_cpp_dropin_selftest(cuda):
 def test_smoke_entry(cuda):
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ------------------------------------------------------------ CLI / PackFile on the GPU
+def _write_mat(path, arr: np.ndarray, colmajor=False):
+    """FPXMAT1 writer from the SPEC text (u32 dtype, rows, cols, u8 layout, 3 pad)."""
+    import struct
+    dt = 0 if arr.dtype == np.float32 else 1
+    rows, cols = arr.shape
+    payload = (arr.T if colmajor else arr).astype("<f4" if dt == 0 else "<f2").tobytes()
+    with open(path, "wb") as f:
+        f.write(b"FPXMAT1\0" + struct.pack("<IIIB3x", dt, rows, cols, 1 if colmajor else 0) + payload)
+
+
+def _read_mat(path) -> np.ndarray:
+    import struct
+    b = open(path, "rb").read()
+    assert b[:8] == b"FPXMAT1\0"
+    dt, rows, cols, lo = struct.unpack_from("<IIIB", b, 8)
+    a = np.frombuffer(b, dtype="<f4" if dt == 0 else "<f2", offset=24).reshape((cols, rows) if lo else (rows, cols))
+    return a.T if lo else a
+
+
+def test_cli_pack_unpack_gemm_check_selftest(cuda, oracle, tmp_path):
+    cli = os.path.join(ROOT, "paper_2401_14112_b200", "build", "fpx")
+    rng = np.random.default_rng(9)
+    w = (rng.standard_normal((150, 200)) * 0.02).astype(np.float32)
+    _write_mat(tmp_path / "w.mat", w)
+    r = subprocess.run([cli, "pack", "--input", str(tmp_path / "w.mat"), "--format", "e3m2", "--output",
+                        str(tmp_path / "w.pack")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    # the file is the library's own pack, byte for byte (same quantize + pack)
+    fpx = _fpx()
+    p = fpx.pack(fpx.quantize_matrix(torch.from_numpy(w).to(cuda), fpx.FpxFormat.e3m2()))
+    assert open(tmp_path / "w.pack", "rb").read() == fpx.serialize_packed(p)
+    # read straight to device == the library's tensors
+    q = fpx.read_pack_file(str(tmp_path / "w.pack"), device=cuda)
+    assert all(bool((a == b).all()) for a, b in zip(q.streams, p.streams)) and bool((q.scales == p.scales).all())
+    # unpack = de-quantised weights (bit-exact vs the oracle)
+    r = subprocess.run([cli, "unpack", "--input", str(tmp_path / "w.pack"), "--output", str(tmp_path / "u.mat")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    got = _read_mat(tmp_path / "u.mat").view(np.uint16)
+    qm = fpx.unpack(p)
+    ref = oracle.dequantize(qm.codes.cpu().numpy(), qm.scales.cpu().numpy().view(np.uint16), 3, 2)
+    assert (got == ref[:150, :200]).all()
+    # gemm --check
+    b = rng.standard_normal((200, 9)).astype(np.float16)
+    _write_mat(tmp_path / "b.mat", b, colmajor=True)
+    r = subprocess.run([cli, "gemm", "--weights", str(tmp_path / "w.pack"), "--activations", str(tmp_path / "b.mat"),
+                        "--output", str(tmp_path / "c.mat"), "--check"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = subprocess.run([cli, "selftest"], capture_output=True, text=True)
+    assert r.returncode == 0 and "selftest: ok" in r.stdout, r.stdout + r.stderr
