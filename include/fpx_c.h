@@ -151,6 +151,25 @@ void fpx_shard_rows(uint32_t rows_p, int rank, int world, uint32_t* tr0, uint32_
 int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32_t* nrows, int world,
                        uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream);
 
+/* ---- K2 with a fused epilogue ---------------------------
+ * The paper positions its kernel as a drop-in linear with fp16 activations
+ * in and out.  fpx_linear_ex computes, per output element,
+ *   C(m, j) = act( sum_k dequant(W)(m, k) * act(k, j) + bias[m] ) + residual(m, j)
+ * in fp32 and stores it as out_dtype (fp16: round-to-nearest-even).  c and
+ * residual share the dtype, the col-major layout and ldc.  epi == NULL is
+ * fpx_linear.  Activations: SiLU x*sigmoid(x), GELU tanh approximation. */
+enum fpx_activation { FPX_ACT_NONE = 0, FPX_ACT_RELU = 1, FPX_ACT_SILU = 2, FPX_ACT_GELU_TANH = 3 };
+typedef struct fpx_epilogue {
+    int out_dtype;          /* FPX_FP32 or FPX_FP16 */
+    const float* bias;      /* rows_p fp32, or NULL */
+    int activation;         /* enum fpx_activation */
+    const void* residual;   /* same dtype / layout / ldc as c, or NULL */
+} fpx_epilogue;
+int fpx_linear_ex(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
+                  uint32_t cols_p, int exp_bits, int man_bits, const uint16_t* act, uint32_t k_act, uint32_t n,
+                  void* c, uint32_t ldc, int split_k, const fpx_epilogue* epi, void* workspace,
+                  size_t workspace_bytes, fpx_stream_t stream);
+
 /* ---- PackFile container (io.hpp:13-41, SPEC.md model-io; host only) ----
  * "FPXPACK1" | u16 version=1 | u8 exp_bits | u8 man_bits | u8 nseg |
  * u8 widths[nseg] (high bits first) | u32 orig_rows, orig_cols, padded_rows,

@@ -23,6 +23,11 @@ _intp = C.POINTER(C.c_int)
 _lib = None
 
 
+class Epilogue(C.Structure):
+    """fpx_epilogue (include/fpx_c.h)."""
+    _fields_ = [("out_dtype", C.c_int), ("bias", C.c_void_p), ("activation", C.c_int), ("residual", C.c_void_p)]
+
+
 class PackHeader(C.Structure):
     """fpx_pack_header (include/fpx_c.h)."""
     _fields_ = [("exp_bits", C.c_int), ("man_bits", C.c_int), ("nseg", C.c_int), ("widths", C.c_int * 3),
@@ -72,6 +77,9 @@ def load(path: str | None = None) -> C.CDLL:
                                  C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
         "fpx_last_error_offset": (C.c_int64, []),
+        "fpx_linear_ex": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int,
+                                    C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
+                                    C.POINTER(Epilogue), C.c_void_p, C.c_size_t, C.c_void_p]),
         "fpx_packfile_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, _intp, C.c_int]),
         "fpx_packfile_encode": (C.c_int, [C.c_int, C.c_int, _intp, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
                                           C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.c_size_t]),

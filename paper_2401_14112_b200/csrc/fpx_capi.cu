@@ -344,10 +344,19 @@ size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_ac
     return ws_layout(rows_p, cols_p, n, split_k, k_act != cols_p).total;
 }
 
-int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p,
-               int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, float* c, uint32_t ldc, int split_k,
-               void* workspace, size_t workspace_bytes, fpx_stream_t stream) {
+static int linear_impl(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
+                       uint32_t cols_p, int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, void* c,
+                       uint32_t ldc, int split_k, void* workspace, size_t workspace_bytes, fpx_stream_t stream,
+                       const fpx_epilogue* epi) {
     if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (epi != nullptr) {
+        if (epi->out_dtype != FPX_FP32 && epi->out_dtype != FPX_FP16)
+            return fail(FPX_ERR_INVALID_VALUE, "epilogue out_dtype must be FPX_FP32 or FPX_FP16");
+        if (epi->activation < FPX_ACT_NONE || epi->activation > FPX_ACT_GELU_TANH)
+            return fail(FPX_ERR_INVALID_VALUE, "unknown epilogue activation %d", epi->activation);
+    }
+    const bool out16 = epi != nullptr && epi->out_dtype == FPX_FP16;
+    const size_t esz = out16 ? 2 : 4;
     int fmt = -1;
     int w[3];
     const int ns = resolve_split(e, m, nullptr, 0, w);
@@ -398,8 +407,16 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
         L.act = a + static_cast<size_t>(n0) * cols_p;
         L.lda = cols_p;
         L.n = (n - n0) < chunk ? (n - n0) : chunk;
-        L.c = c + static_cast<size_t>(n0) * ldc;
+        L.c = reinterpret_cast<float*>(static_cast<uint8_t*>(c) + static_cast<size_t>(n0) * ldc * esz);
         L.ldc = ldc;
+        if (epi != nullptr) {
+            L.out_f16 = out16 ? 1u : 0u;
+            L.bias = epi->bias;
+            L.act_fn = static_cast<uint32_t>(epi->activation);
+            L.resid = epi->residual == nullptr
+                          ? nullptr
+                          : static_cast<const uint8_t*>(epi->residual) + static_cast<size_t>(n0) * ldc * esz;
+        }
         L.split = split_k;
         L.ws = part;
         L.counters = counters;
@@ -411,6 +428,21 @@ int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, 
         if (err != cudaSuccess) return cuda_fail(err, "fpx_linear_kernel launch");
     }
     return FPX_OK;
+}
+
+int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p,
+               int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, float* c, uint32_t ldc, int split_k,
+               void* workspace, size_t workspace_bytes, fpx_stream_t stream) {
+    return linear_impl(streams, nseg, scales, rows_p, cols_p, e, m, act, k_act, n, c, ldc, split_k, workspace,
+                       workspace_bytes, stream, nullptr);
+}
+
+int fpx_linear_ex(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
+                  uint32_t cols_p, int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, void* c,
+                  uint32_t ldc, int split_k, const fpx_epilogue* epi, void* workspace, size_t workspace_bytes,
+                  fpx_stream_t stream) {
+    return linear_impl(streams, nseg, scales, rows_p, cols_p, e, m, act, k_act, n, c, ldc, split_k, workspace,
+                       workspace_bytes, stream, epi);
 }
 
 // ---------------------------------------------------------------- multi-GPU

@@ -34,7 +34,7 @@ struct LinearLaunch {
     const uint16_t* act;       // col-major activations, row j at act + j*lda, K == cols_p
     uint32_t lda;              // >= cols_p, multiple of 8
     uint32_t n;                // batch (1..256)
-    float* c;                  // col-major output, element (m, j) at c[j*ldc + m]
+    float* c;                  // col-major output, element (m, j) at c[j*ldc + m] (fp16 when out_f16)
     uint32_t ldc;
     int split;                 // K chunks per 128-row tile (>= 1)
     float* ws;                 // split > 1: partial sums
@@ -42,6 +42,11 @@ struct LinearLaunch {
     int grid;                  // persistent CTAs (0 = auto)
     unsigned long long* trace; // debug: per-stage clock64 trace of CTA 0 (7 events x 512 stages), or null
     volatile unsigned long long* prog;  // debug: mapped host progress words (FPX_LINEAR_TRACE=3), or null
+    // fused epilogue (fpx_linear_ex): C = act(A.B + bias) + residual, stored fp32 or fp16
+    uint32_t out_f16;
+    const float* bias;         // rows_p, or null
+    uint32_t act_fn;           // 0 none, 1 relu, 2 silu, 3 gelu (tanh)
+    const void* resid;         // same dtype / layout / ldc as C, or null
 };
 
 cudaError_t launch_linear(const LinearLaunch& p, cudaStream_t st);

@@ -30,6 +30,7 @@
 //                      (conflict-free jagged rows), runs the register-level
 //                      de-quantisation and tcgen05.st's the fp16 A fragments
 //                      (16x128b shape == mma A-fragment register order).
+#include <cuda_fp16.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -78,7 +79,37 @@ struct KParams {
     unsigned long long* trace;  // optional per-stage clock trace of CTA 0 (fpx_debug_trace), else null
     volatile unsigned long long* prog;  // debug: mapped host memory, per (CTA, warp) current wait, else null
     uint32_t pdl;  // launched with programmatic stream serialization (weights may be prefetched before the dependency wait)
+    uint32_t epi;      // any fused epilogue op below (uniform branch at every C store)
+    uint32_t out_f16;  // C stored as fp16
+    const float* bias;
+    uint32_t act;      // 0 none, 1 relu, 2 silu, 3 gelu (tanh)
+    const void* resid;
 };
+
+// Every final C element goes through here (split-K partials do not): the
+// fused epilogue of fpx_linear_ex, C = act(acc + bias[m]) + residual, in
+// fp32, then stored as fp32 or fp16 (RNE).
+__device__ __forceinline__ void c_store(const KParams& p, uint32_t m, uint32_t col, float v) {
+    const size_t i = static_cast<size_t>(col) * p.ldc + m;
+    if (p.epi) {
+        if (p.bias != nullptr) v += __ldg(&p.bias[m]);
+        if (p.act == 1u) {
+            v = fmaxf(v, 0.0f);
+        } else if (p.act != 0u) {
+            // SiLU v*sigmoid(v); GELU(tanh) 0.5v(1+tanh(u)) == v*sigmoid(2u),
+            // u = sqrt(2/pi)(v + 0.044715 v^3): one exp either way
+            const float z = p.act == 2u ? v : 1.5957691216057308f * v * (1.0f + 0.044715f * v * v);
+            v = __fdividef(v, 1.0f + __expf(-z));
+        }
+        if (p.resid != nullptr)
+            v += p.out_f16 ? __half2float(static_cast<const __half*>(p.resid)[i]) : static_cast<const float*>(p.resid)[i];
+        if (p.out_f16) {
+            reinterpret_cast<__half*>(p.c)[i] = __float2half_rn(v);
+            return;
+        }
+    }
+    p.c[i] = v;
+}
 
 // Debug (FPX_LINEAR_TRACE=3): record, in mapped host memory the host can read
 // while a launch is stuck, which barrier each warp is waiting on.
@@ -389,7 +420,7 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
                         const uint32_t col = c0 + j;
                         if (col < p.n) {
                             if (p.split == 1) {
-                                if (row_ok) p.c[static_cast<size_t>(col) * p.ldc + m] = __uint_as_float(v[j]);
+                                if (row_ok) c_store(p, m, col, __uint_as_float(v[j]));
                             } else {
                                 part[static_cast<size_t>(col) * kTileM + row_l] = __uint_as_float(v[j]);
                             }
@@ -423,7 +454,7 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
                         if (row_ok) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
-                                if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = acc[j];
+                                if (c0 + j < p.n) c_store(p, m, c0 + j, acc[j]);
                         }
                     }
                     if (lane == 0) p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
@@ -659,7 +690,7 @@ __device__ __forceinline__ void final_split_reduce(const KParams& p, const uint3
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-                if (4 * sl + j < p.n) p.c[static_cast<size_t>(4 * sl + j) * p.ldc + m] = a4[j];
+                if (4 * sl + j < p.n) c_store(p, m, 4 * sl + j, a4[j]);
         }
     }
 }
@@ -891,7 +922,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     if (c0 < p.n && row_ok) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = __uint_as_float(v[j]);
+                            if (c0 + j < p.n) c_store(p, m, c0 + j, __uint_as_float(v[j]));
                     }
                 } else if (c0 < p.n) {
                     // columns >= n hold exact zeros (zero-filled activations)
@@ -957,7 +988,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
-                                if (c0 + j < p.n) p.c[static_cast<size_t>(c0 + j) * p.ldc + m] = a4[j];
+                                if (c0 + j < p.n) c_store(p, m, c0 + j, a4[j]);
                         }
                     }
                     if (q == 0 && lane == 0) trace_cta(p, 8);
@@ -1308,6 +1339,11 @@ cudaError_t launch_linear(const LinearLaunch& L, cudaStream_t st) {
     kp.scales = L.scales;
     kp.c = L.c;
     kp.ldc = L.ldc;
+    kp.out_f16 = L.out_f16;
+    kp.bias = L.bias;
+    kp.act = L.act_fn;
+    kp.resid = L.resid;
+    kp.epi = (L.out_f16 || L.bias != nullptr || L.act_fn != 0 || L.resid != nullptr) ? 1u : 0u;
     kp.rows_p = L.rows_p;
     kp.tile_rows = L.rows_p / 64;
     kp.kt = L.cols_p / 64;

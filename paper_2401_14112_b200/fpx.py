@@ -36,7 +36,7 @@ __all__ = [
     "ErrorCode", "FpxError", "FpxFormat", "SplitScheme", "QuantizedMatrix", "PackedWeights",
     "quantize_matrix", "pack", "unpack", "dequantize", "gemm_packed", "fp6_linear", "effective_scale",
     "linear_workspace", "default_split", "serialize_packed", "deserialize_packed", "write_pack_file",
-    "read_pack_file",
+    "read_pack_file", "linear",
 ]
 
 
@@ -399,6 +399,49 @@ def read_pack_file(path: str, device: str | torch.device = "cuda") -> PackedWeig
     ptrs = (C.c_void_p * h.nseg)(*[t.data_ptr() for t in streams])
     _check(L.fpx_packfile_load(path.encode(), C.byref(h), scales.data_ptr(), ptrs, _stream(dev)))
     return _from_header(h, scales, streams)
+
+
+ACTIVATIONS = {None: 0, "none": 0, "relu": 1, "silu": 2, "gelu_tanh": 3}
+
+
+def linear(act: torch.Tensor, p: PackedWeights, *, bias: torch.Tensor | None = None, activation: str | None = None,
+           residual: torch.Tensor | None = None, out_dtype: torch.dtype = torch.float16, split_k: int = 0,
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """The fused linear with the fp16-output epilogue (fpx_linear_ex):
+    out[n, m] = activation(act[n] . W[m] + bias[m]) + residual[n, m], computed
+    in fp32, stored as out_dtype (fp16 RNE or fp32).  act: [N, K] fp16 with K ==
+    p.cols or p.orig_cols; bias: [p.rows] fp32 (or [orig_rows], zero-padded);
+    residual: [N, p.rows] of out_dtype."""
+    L = _lib.load()
+    if act.dtype != torch.float16 or act.dim() != 2 or not act.is_cuda:
+        raise FpxError(3, "error[invalid-value] activations must be a CUDA fp16 [N, K] tensor")
+    if out_dtype not in (torch.float16, torch.float32):
+        raise FpxError(3, "error[invalid-value] out_dtype must be float16 or float32")
+    act = act.contiguous()
+    n, k = act.shape
+    dev = act.device
+    if out is None:
+        out = torch.empty((n, p.rows), dtype=out_dtype, device=dev)
+    if out.dtype != out_dtype or out.shape != (n, p.rows) or not out.is_contiguous():
+        raise FpxError(5, "error[shape-mismatch] out must be contiguous [N, rows_p] of out_dtype")
+    if bias is not None:
+        bias = bias.to(device=dev, dtype=torch.float32).contiguous()
+        if bias.numel() < p.rows:
+            bias = torch.nn.functional.pad(bias, (0, p.rows - bias.numel()))
+    if residual is not None:
+        if residual.dtype != out_dtype or residual.shape != (n, p.rows):
+            raise FpxError(5, "error[shape-mismatch] residual must be [N, rows_p] of out_dtype")
+        residual = residual.contiguous()
+    if activation not in ACTIVATIONS:
+        raise FpxError(3, f"error[invalid-value] activation must be one of {sorted(k for k in ACTIVATIONS if k)}")
+    epi = _lib.Epilogue(1 if out_dtype == torch.float16 else 0, _ptr(bias), ACTIVATIONS[activation], _ptr(residual))
+    ws_bytes = int(L.fpx_linear_workspace_size(p.rows, p.cols, k, n, split_k))
+    ws = linear_workspace(dev, ws_bytes)
+    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+    _check(L.fpx_linear_ex(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                           p.format.man_bits, act.data_ptr(), k, n, out.data_ptr(), p.rows, split_k, C.byref(epi),
+                           _ptr(ws), ws_bytes, _stream(dev)))
+    return out
 
 
 def fp6_linear(act: torch.Tensor, packed: PackedWeights, **kw) -> torch.Tensor:

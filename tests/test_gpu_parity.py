@@ -376,3 +376,55 @@ def test_cli_pack_unpack_gemm_check_selftest(cuda, oracle, tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     r = subprocess.run([cli, "selftest"], capture_output=True, text=True)
     assert r.returncode == 0 and "selftest: ok" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------ fused epilogue (fpx_linear_ex)
+@pytest.mark.parametrize("n", [1, 16, 48, 100])
+@pytest.mark.parametrize("split", [0, 1, 3])
+def test_linear_fused_epilogue(cuda, n, split):
+    fpx = _fpx()
+    import torch.nn.functional as Fn
+    rng = np.random.default_rng(n * 7 + split)
+    rows, cols = 300, 704
+    w = torch.from_numpy((rng.standard_normal((rows, cols)) * 0.05).astype(np.float32)).to(cuda)
+    p = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
+    W = fpx.dequantize(p).float()
+    x = torch.from_numpy(rng.standard_normal((n, cols)).astype(np.float16)).to(cuda)
+    base = x.float() @ W.t()  # [n, rows_p]
+    bias = torch.from_numpy(rng.standard_normal(rows).astype(np.float32)).to(cuda)  # orig rows: zero-padded
+    bias_p = Fn.pad(bias, (0, p.rows - rows))
+    res = torch.from_numpy(rng.standard_normal((n, p.rows)).astype(np.float16)).to(cuda)
+    acts = {"none": lambda t: t, "relu": torch.relu, "silu": Fn.silu, "gelu_tanh": lambda t: Fn.gelu(t, approximate="tanh")}
+    for name, f in acts.items():
+        y = fpx.linear(x, p, bias=bias, activation=name, residual=res, split_k=split)
+        assert y.dtype == torch.float16 and y.shape == (n, p.rows)
+        ref = f(base + bias_p) + res.float()
+        nrm = ref.abs().amax(dim=1, keepdim=True).clamp_min(1e-6)
+        err = ((y.float() - ref).abs() / nrm).max().item()
+        assert err < 2e-3, (name, err)  # fp16 output rounding (2^-11) + the 1e-2 bar's fp32 part, far inside
+    y32 = fpx.linear(x, p, out_dtype=torch.float32, split_k=split)
+    c = fpx.gemm_packed(p, x, split_k=split)
+    assert torch.equal(y32, c)  # no epilogue ops: the same bits as fpx_linear
+
+
+def test_torch_custom_op_and_module(cuda):
+    from paper_2401_14112_b200.ops import FpxLinear
+    torch.manual_seed(0)
+    lin = torch.nn.Linear(256, 200, bias=True).to(cuda)
+    m = FpxLinear(lin.weight, lin.bias, activation="silu")
+    x = torch.randn(3, 5, 256, device=cuda).half()
+    y = m(x)
+    assert y.shape == (3, 5, 200) and y.dtype == torch.float16
+    p = torch.ops.fpx.linear  # registered
+    W = _fpx().dequantize(_fpx().PackedWeights(m.fmt, _fpx().SplitScheme.for_format(m.fmt), m.rows_p, m.cols_p,
+                                                 m.rows_p, m.orig_cols, [m.stream_hi, m.stream_lo], m.scales)).float()
+    ref = torch.nn.functional.silu(x.reshape(-1, 256).float() @ W[:200].t() + lin.bias.float())
+    assert ((y.reshape(-1, 200).float() - ref).abs().max() / ref.abs().max()).item() < 2e-3
+    # fake/meta implementation: shape propagation without the kernel
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    x2 = x.reshape(-1, 256)
+    with FakeTensorMode() as mode:
+        fx = mode.from_tensor(x2)
+        out = p(fx, mode.from_tensor(m.stream_hi), mode.from_tensor(m.stream_lo), mode.from_tensor(m.scales),
+                3, 2, m.rows_p, m.cols_p, m.orig_cols, None, "none")
+        assert out.shape == (15, m.rows_p)
