@@ -94,6 +94,16 @@ size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width);
 int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int exp_bits, int man_bits,
                  uint8_t* codes, uint16_t* scales, uint64_t* status_dev, fpx_stream_t stream);
 
+/* ---- K0+K1 fused: quantize straight into the packed streams
+ * Bit-exact with fpx_quantize followed by fpx_prepack (same scales, same
+ * stream bytes, same first-failing-row errors), without the code matrix in
+ * HBM: pass 1 computes row scales, pass 2 encodes each 64x64 tile into
+ * shared memory and packs it.  streams[i]: fpx_stream_bytes(pad64(rows),
+ * pad64(cols), widths[i]); widths/nseg NULL/0 -> the format's preset. */
+int fpx_quantize_pack(const void* w, int dtype, uint32_t rows, uint32_t cols, int exp_bits, int man_bits,
+                      const int* widths, int nseg, uint8_t* const* streams, uint16_t* scales, uint64_t* status_dev,
+                      fpx_stream_t stream);
+
 /* ---- K1: pre-pack (prepack.cpp:153-209) -------------------------------
  * codes: rows_p x cols_p (multiples of 64); widths/nseg: the split (NULL ->
  * the format's preset, format.cpp:59-69); streams[i]: device buffers of

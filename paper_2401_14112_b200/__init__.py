@@ -8,7 +8,7 @@ tcgen05 GEMM behind the reference's API (see fpx.py) and a C-ABI
 from . import _lib  # noqa: F401
 from .fpx import (  # noqa: F401
     ErrorCode, FpxError, FpxFormat, PackedWeights, QuantizedMatrix, SplitScheme, default_split, dequantize,
-    deserialize_packed, effective_scale, fp6_linear, gemm_packed, linear, pack, quantize_matrix, read_pack_file,
+    deserialize_packed, effective_scale, fp6_linear, gemm_packed, linear, pack, quantize_pack, quantize_matrix, read_pack_file,
     serialize_packed, unpack, write_pack_file,
 )
 from . import shard  # noqa: F401,E402

@@ -249,6 +249,50 @@ int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, 
                 15 - bias_of(e));
 }
 
+// ---------------------------------------------------------------- K0+K1 fused
+int fpx_quantize_pack(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, int m, const int* widths,
+                      int nseg, uint8_t* const* streams, uint16_t* scales, uint64_t* status_dev,
+                      fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (dtype != FPX_FP32 && dtype != FPX_FP16)
+        return fail(FPX_ERR_INVALID_VALUE, "quantize expects a row-major fp32 matrix");
+    if (rows == 0 || cols == 0) return fail(FPX_ERR_SHAPE_MISMATCH, "empty matrix");
+    int wv[3];
+    const int ns = resolve_split(e, m, widths, nseg, wv);
+    if (ns <= 0) return fail(FPX_ERR_UNSUPPORTED_SPLIT, "segment widths must be 1, 2 or 4 and sum to %d", 1 + e + m);
+    if (!w || !scales || !streams) return fail(FPX_ERR_INVALID_VALUE, "null buffer");
+    for (int i = 0; i < ns; ++i)
+        if (!streams[i]) return fail(FPX_ERR_INVALID_VALUE, "null stream buffer");
+    if (int st = check_device(false)) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const uint32_t rows_p = fpx_pad64(rows), cols_p = fpx_pad64(cols);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
+    uint8_t* scratch = nullptr;  // [status (own) | row skip flags]
+    const size_t skip_off = 16;
+    FPX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), skip_off + rows_p, s));
+    const bool own = status == nullptr;
+    if (own) status = reinterpret_cast<unsigned long long*>(scratch);
+    FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    const double maxrep = static_cast<double>(fpx_max_representable(e, m));
+    uint8_t* sp[3] = {streams[0], ns > 1 ? streams[1] : nullptr, ns > 2 ? streams[2] : nullptr};
+    FPX_CUDA(launch_quantize_pack(w, dtype, rows, cols, rows_p, cols_p, e, m, maxrep, scales, status,
+                                  scratch + skip_off, ns, wv, sp, s));
+    if (!own) {
+        FPX_CUDA(cudaFreeAsync(scratch, s));
+        return FPX_OK;
+    }
+    unsigned long long host = 0;
+    FPX_CUDA(cudaMemcpyAsync(&host, status, sizeof host, cudaMemcpyDeviceToHost, s));
+    FPX_CUDA(cudaFreeAsync(scratch, s));
+    FPX_CUDA(cudaStreamSynchronize(s));
+    if (host == ~0ull) return FPX_OK;
+    const unsigned long long row = host >> 8;
+    const int code = static_cast<int>(host & 0xffu);
+    if (code == FPX_ERR_INVALID_VALUE) return fail(code, "row %llu contains NaN", row);
+    return fail(code, "row %llu scale does not fit in fp16 (or its 2^%d-folded effective scale overflows)", row,
+                15 - bias_of(e));
+}
+
 // ---------------------------------------------------------------- K1
 int fpx_prepack(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int e, int m,
                 const int* widths, int nseg, uint8_t* const* streams, fpx_stream_t stream) {

@@ -50,14 +50,21 @@ __device__ __forceinline__ float load_w<uint16_t>(const uint16_t* p) {
     return __half2float(__ushort_as_half(*p));  // exact (codec.cpp:35-40)
 }
 
+// codes == nullptr: row scales, status and the per-row skip flag only (pass 1
+// of the fused quantize+pack, whose tile kernel encodes and packs).
 template <typename T>
 __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, uint32_t rows,
                                                        uint32_t cols, uint32_t cols_p, int e, int m,
                                                        double maxrep, uint8_t* __restrict__ codes,
                                                        uint16_t* __restrict__ scales,
-                                                       unsigned long long* __restrict__ status) {
+                                                       unsigned long long* __restrict__ status,
+                                                       uint8_t* __restrict__ row_skip) {
     const uint32_t r = blockIdx.x;
-    uint8_t* out = codes + static_cast<size_t>(r) * cols_p;
+    uint8_t* out = codes ? codes + static_cast<size_t>(r) * cols_p : nullptr;
+    if (codes == nullptr && r >= rows) {
+        if (threadIdx.x == 0) scales[r] = 0x3c00u, row_skip[r] = 1;
+        return;
+    }
     __shared__ float red[8];
     __shared__ int nan_flag;
     __shared__ double s_val;
@@ -111,8 +118,10 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
             s16 = 0x3c00u;
         }
         scales[r] = s16;
+        if (row_skip) row_skip[r] = static_cast<uint8_t>(skip);
         s_val = static_cast<double>(__half2float(__ushort_as_half(s16)));
     }
+    if (codes == nullptr) return;
     __syncthreads();
     const int bias = (1 << (e - 1)) - 1;
     const double sv = s_val;
@@ -188,6 +197,70 @@ __global__ void __launch_bounds__(32 * kPackWarps) prepack_kernel(const uint8_t*
                     code_rc(t, it * 4u + q, rr, cc);
                     const uint32_t v = (static_cast<uint32_t>(ts[rr * 64u + cc]) >> low) & vmask;
                     word |= v << (8u * kLane[q] + 8u - w * (g + 1u));
+                }
+            }
+            reinterpret_cast<uint32_t*>(blk)[j * 32u + t] = word;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K0+K1 fused
+// Pass 2 of fpx_quantize_pack: one warp per 64x64 tile encodes its codes
+// straight from the weights (the same fp64 RNE encode of double(w) / s as
+// quantize_kernel, codec.cpp:168-170, with the row scales and skip flags of
+// pass 1) into shared memory, then packs them exactly like prepack_kernel.
+// The code matrix never exists in HBM.
+template <typename T>
+__global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T* __restrict__ w, uint32_t rows,
+                                                                        uint32_t cols, uint32_t cols_p,
+                                                                        uint32_t ntiles, int e, int m,
+                                                                        double maxrep,
+                                                                        const uint16_t* __restrict__ scales,
+                                                                        const uint8_t* __restrict__ row_skip,
+                                                                        int bits, SplitDesc sd) {
+    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * 64];
+    const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
+    const uint32_t tile = blockIdx.x * kPackWarps + warp;
+    if (tile >= ntiles) return;
+    const uint32_t gc = cols_p / 64u;
+    const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
+    uint8_t* ts = tile_s[warp];
+    const int bias = (1 << (e - 1)) - 1;
+    // two rows per pass: lanes 0-15 row 2i, 16-31 row 2i+1, 4 consecutive columns each
+    for (uint32_t i = 0; i < 32u; ++i) {
+        const uint32_t rr = 2u * i + (t >> 4), cc = (t & 15u) * 4u;
+        const uint32_t r = r0 + rr;
+        uint32_t packed4 = 0;
+        if (r < rows && !row_skip[r]) {
+            const double sv = static_cast<double>(__half2float(__ushort_as_half(scales[r])));
+            const T* row = w + static_cast<size_t>(r) * cols;
+#pragma unroll
+            for (uint32_t q = 0; q < 4u; ++q) {
+                const uint32_t c = c0 + cc + q;
+                if (c < cols)
+                    packed4 |= encode_dev(static_cast<double>(load_w(row + c)) / sv, e, m, bias, maxrep) << (8u * q);
+            }
+        }
+        *reinterpret_cast<uint32_t*>(ts + rr * 64u + cc) = packed4;
+    }
+    __syncwarp();
+    int low = bits;
+    for (int sg = 0; sg < sd.nseg; ++sg) {
+        const int wd = sd.width[sg];
+        low -= wd;
+        const uint32_t per_word = 8u / wd, nwords = 4u * wd;
+        const uint32_t vmask = (1u << wd) - 1u;
+        uint8_t* blk = sd.stream[sg] + static_cast<size_t>(tile) * 512u * wd;
+        for (uint32_t j = 0; j < nwords; ++j) {
+            uint32_t word = 0;
+            for (uint32_t g = 0; g < per_word; ++g) {
+                const uint32_t it = j * per_word + g;
+#pragma unroll
+                for (uint32_t q = 0; q < 4u; ++q) {
+                    uint32_t rr, cc;
+                    code_rc(t, it * 4u + q, rr, cc);
+                    const uint32_t v = (static_cast<uint32_t>(ts[rr * 64u + cc]) >> low) & vmask;
+                    word |= v << (8u * kLane[q] + 8u - wd * (g + 1u));
                 }
             }
             reinterpret_cast<uint32_t*>(blk)[j * 32u + t] = word;
@@ -384,10 +457,33 @@ cudaError_t launch_quantize(const void* w, int w_dtype, uint32_t rows, uint32_t 
                             uint16_t* scales, unsigned long long* status, cudaStream_t st) {
     if (w_dtype == 0)
         quantize_kernel<float><<<rows_p, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, cols_p, e, m,
-                                                       maxrep, codes, scales, status);
+                                                       maxrep, codes, scales, status, nullptr);
     else
         quantize_kernel<uint16_t><<<rows_p, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, cols_p,
-                                                          e, m, maxrep, codes, scales, status);
+                                                          e, m, maxrep, codes, scales, status, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize_pack(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
+                                 uint32_t cols_p, int e, int m, double maxrep, uint16_t* scales,
+                                 unsigned long long* status, uint8_t* row_skip, int nseg, const int* widths,
+                                 uint8_t* const* streams, cudaStream_t st) {
+    const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
+    const int bits = 1 + e + m;
+    const SplitDesc sd = make_sd(nseg, widths, streams);
+    const uint32_t grid = (ntiles + kPackWarps - 1) / kPackWarps;
+    if (w_dtype == 0) {
+        quantize_kernel<float><<<rows_p, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, cols_p, e, m,
+                                                       maxrep, nullptr, scales, status, row_skip);
+        quantize_pack_kernel<float><<<grid, 32 * kPackWarps, 0, st>>>(
+            static_cast<const float*>(w), rows, cols, cols_p, ntiles, e, m, maxrep, scales, row_skip, bits, sd);
+    } else {
+        quantize_kernel<uint16_t><<<rows_p, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, cols_p, e,
+                                                          m, maxrep, nullptr, scales, status, row_skip);
+        quantize_pack_kernel<uint16_t><<<grid, 32 * kPackWarps, 0, st>>>(static_cast<const uint16_t*>(w), rows,
+                                                                         cols, cols_p, ntiles, e, m, maxrep,
+                                                                         scales, row_skip, bits, sd);
+    }
     return cudaGetLastError();
 }
 

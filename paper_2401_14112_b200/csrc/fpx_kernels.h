@@ -10,6 +10,10 @@
 cudaError_t launch_quantize(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
                             uint32_t cols_p, int e, int m, double maxrep, uint8_t* codes,
                             uint16_t* scales, unsigned long long* status, cudaStream_t st);
+cudaError_t launch_quantize_pack(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
+                                 uint32_t cols_p, int e, int m, double maxrep, uint16_t* scales,
+                                 unsigned long long* status, uint8_t* row_skip, int nseg, const int* widths,
+                                 uint8_t* const* streams, cudaStream_t st);
 cudaError_t launch_prepack(const uint8_t* codes, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,
                            const int* widths, uint8_t* const* streams, cudaStream_t st);
 cudaError_t launch_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,

@@ -36,7 +36,7 @@ __all__ = [
     "ErrorCode", "FpxError", "FpxFormat", "SplitScheme", "QuantizedMatrix", "PackedWeights",
     "quantize_matrix", "pack", "unpack", "dequantize", "gemm_packed", "fp6_linear", "effective_scale",
     "linear_workspace", "default_split", "serialize_packed", "deserialize_packed", "write_pack_file",
-    "read_pack_file", "linear",
+    "read_pack_file", "linear", "quantize_pack",
 ]
 
 
@@ -247,6 +247,28 @@ def pack(q: QuantizedMatrix, split: SplitScheme | None = None) -> PackedWeights:
                          q.format.man_bits, wid, len(split.widths), ptrs, _stream(dev)))
     return PackedWeights(q.format, split, q.rows, q.cols, q.orig_rows or q.rows, q.orig_cols or q.cols, streams,
                          q.scales.clone())
+
+
+def quantize_pack(m: torch.Tensor, fmt: FpxFormat, split: SplitScheme | None = None) -> PackedWeights:
+    """pack(quantize_matrix(m, fmt)) in one fused GPU pass (fpx_quantize_pack):
+    bit-exact with the two-step path, without the code matrix in HBM."""
+    L = _lib.load()
+    if m.dim() != 2 or not m.is_cuda or m.dtype not in (torch.float32, torch.float16):
+        raise FpxError(3, "error[invalid-value] quantize expects a row-major fp32 matrix")
+    rows, cols = m.shape
+    if rows == 0 or cols == 0:
+        raise FpxError(5, "error[shape-mismatch] empty matrix")
+    m = m.contiguous()
+    split = split or SplitScheme.for_format(fmt)
+    rp, cp = pad64(rows), pad64(cols)
+    streams = [torch.empty(L.fpx_stream_bytes(rp, cp, w), dtype=torch.uint8, device=m.device) for w in split.widths]
+    scales = torch.empty((rp,), dtype=torch.int16, device=m.device)
+    wid = (C.c_int * len(split.widths))(*split.widths)
+    ptrs = (C.c_void_p * len(streams))(*[s.data_ptr() for s in streams])
+    _check(L.fpx_quantize_pack(m.data_ptr(), 0 if m.dtype == torch.float32 else 1, rows, cols, fmt.exp_bits,
+                               fmt.man_bits, wid, len(split.widths), ptrs, scales.data_ptr(), None,
+                               _stream(m.device)))
+    return PackedWeights(fmt, split, rp, cp, rows, cols, streams, scales)
 
 
 def unpack(p: PackedWeights) -> QuantizedMatrix:

@@ -428,3 +428,45 @@ def test_torch_custom_op_and_module(cuda):
         out = p(fx, mode.from_tensor(m.stream_hi), mode.from_tensor(m.stream_lo), mode.from_tensor(m.scales),
                 3, 2, m.rows_p, m.cols_p, m.orig_cols, None, "none")
         assert out.shape == (15, m.rows_p)
+
+
+# ------------------------------------------------------------ fused quantize + pack
+@pytest.mark.parametrize("e,m", [(3, 2), (2, 3), (2, 2), (4, 3), (2, 1)])
+@pytest.mark.parametrize("shape", [(64, 64), (100, 150), (333, 517)])
+def test_quantize_pack_fused_bit_exact(cuda, e, m, shape):
+    fpx = _fpx()
+    rng = np.random.default_rng(shape[0] + 10 * e + m)
+    w = (rng.standard_normal(shape) * rng.choice([1e-3, 0.02, 3.0], size=(shape[0], 1))).astype(np.float32)
+    w[1] = 0.0
+    w[2] = -0.0                           # all -0.0 row: skipped (codes 0) like quantize_matrix
+    w[3, ::7] = -0.0
+    fmt = fpx.FpxFormat(e, m)
+    for dt in (torch.float32, torch.float16):
+        wt = torch.from_numpy(w).to(cuda).to(dt)
+        two = fpx.pack(fpx.quantize_matrix(wt, fmt))
+        one = fpx.quantize_pack(wt, fmt)
+        assert torch.equal(one.scales, two.scales)
+        for a, b in zip(one.streams, two.streams):
+            assert torch.equal(a, b)
+
+
+def test_quantize_pack_fused_errors_and_size(cuda):
+    fpx = _fpx()
+    w = torch.randn(300, 200, device=cuda)
+    w[77, 3] = float("nan")
+    w[120, 0] = float("nan")
+    with pytest.raises(fpx.FpxError) as ei:
+        fpx.quantize_pack(w, fpx.FpxFormat.e3m2())
+    assert ei.value.code == fpx.ErrorCode.InvalidValue and "row 77" in str(ei.value)
+    w = torch.randn(64, 64, device=cuda)
+    w[5] = 3e38
+    with pytest.raises(fpx.FpxError) as ei:
+        fpx.quantize_pack(w, fpx.FpxFormat.e3m2())
+    assert ei.value.code == fpx.ErrorCode.ScaleOverflow
+    # llama-65B size: bit-exact with the two-step path
+    g = torch.Generator(device=cuda)
+    g.manual_seed(1)
+    w = torch.randn(8192, 22016, device=cuda, generator=g) * 0.02
+    one = fpx.quantize_pack(w, fpx.FpxFormat.e3m2())
+    two = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
+    assert torch.equal(one.scales, two.scales) and all(torch.equal(a, b) for a, b in zip(one.streams, two.streams))
