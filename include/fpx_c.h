@@ -161,6 +161,23 @@ void fpx_shard_rows(uint32_t rows_p, int rank, int world, uint32_t* tr0, uint32_
 int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32_t* nrows, int world,
                        uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, fpx_stream_t stream);
 
+/* Sharded linear (SURVEY §8b fpx_linear_sharded, §8e): rank `rank` of
+ * `world` holds tile-rows fpx_shard_rows(rows_p, rank, world) of the packed
+ * weight (shard_streams / shard_scales = that contiguous byte range, zero
+ * copy); every rank passes the same activations and receives the FULL
+ * col-major C (rows_p x n, ldc).  The shard runs with the full problem's
+ * split_k (0 -> fpx_linear_default_split(rows_p, cols_p, n)), so its rows are
+ * bit-identical to a 1-GPU call; the slices are all-gathered over NVLink
+ * with ncclAllGather on `stream` (nccl_comm: the caller's ncclComm_t, from
+ * the NCCL already loaded in the process -- resolved at run time, no link
+ * dependency) and scattered into C.  world == 1 needs no communicator. */
+size_t fpx_linear_sharded_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int world,
+                                         int split_k);
+int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint16_t* shard_scales, uint32_t rows_p,
+                       uint32_t cols_p, int exp_bits, int man_bits, const uint16_t* act, uint32_t k_act, uint32_t n,
+                       float* c, uint32_t ldc, int split_k, int rank, int world, void* nccl_comm, void* workspace,
+                       size_t workspace_bytes, fpx_stream_t stream);
+
 /* ---- K2 with a fused epilogue ---------------------------
  * The paper positions its kernel as a drop-in linear with fp16 activations
  * in and out.  fpx_linear_ex computes, per output element,

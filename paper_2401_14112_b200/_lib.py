@@ -65,6 +65,11 @@ def load(path: str | None = None) -> C.CDLL:
         "fpx_stream_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_int]),
         "fpx_quantize": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
+        "fpx_linear_sharded_workspace_size": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                                        C.c_int]),
+        "fpx_linear_sharded": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int,
+                                         C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,
+                                         C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
         "fpx_quantize_pack": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_int, _intp, C.c_int,
                                         C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_void_p]),
         "fpx_prepack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, _intp, C.c_int,

@@ -3,6 +3,7 @@
 // workspace carving, and dispatch to the sm_100a kernels.  No exception and
 // no host compute fallback: if the device or a kernel is unavailable the
 // call fails with FPX_ERR_DEVICE / FPX_ERR_CUDA.
+#include <dlfcn.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -512,6 +513,79 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
     if (int st = check_device(false)) return st;
     FPX_CUDA(launch_gather_permute(gathered, row0, nrows, world, m_slot, n, c, ldc,
                                    reinterpret_cast<cudaStream_t>(stream)));
+    return FPX_OK;
+}
+
+// ---------------------------------------------------------------- sharded linear
+// NCCL is resolved at call time from the process (dlsym RTLD_DEFAULT, e.g.
+// torch's NCCL), else libnccl.so.2: the ncclComm_t the caller passes must
+// come from the very library whose ncclAllGather runs, and libfpx_b200.so
+// carries no link-time NCCL dependency.
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+static nccl_allgather_fn nccl_allgather() {
+    static nccl_allgather_fn fn = [] {
+        void* f = dlsym(RTLD_DEFAULT, "ncclAllGather");
+        if (f == nullptr) {
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (h != nullptr) f = dlsym(h, "ncclAllGather");
+        }
+        return reinterpret_cast<nccl_allgather_fn>(f);
+    }();
+    return fn;
+}
+
+static uint32_t shard_slot_rows(uint32_t rows_p, int world) {
+    const uint32_t trs = rows_p / 64u;
+    return (trs + static_cast<uint32_t>(world) - 1u) / static_cast<uint32_t>(world) * 64u;
+}
+
+size_t fpx_linear_sharded_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int world,
+                                         int split_k) {
+    if (world <= 0) world = 1;
+    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
+    const uint32_t slot = shard_slot_rows(rows_p, world);
+    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
+    return lin + align256(size_t(slot) * n * 4) + align256(size_t(world) * slot * n * 4);
+}
+
+int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint16_t* shard_scales, uint32_t rows_p,
+                       uint32_t cols_p, int e, int m, const uint16_t* act, uint32_t k_act, uint32_t n, float* c,
+                       uint32_t ldc, int split_k, int rank, int world, void* nccl_comm, void* workspace,
+                       size_t workspace_bytes, fpx_stream_t stream) {
+    if (world <= 0 || rank < 0 || rank >= world) return fail(FPX_ERR_INVALID_VALUE, "rank %d of world %d", rank, world);
+    if (rows_p == 0 || rows_p % 64) return fail(FPX_ERR_SHAPE_MISMATCH, "packed rows must be a multiple of 64");
+    if (ldc < rows_p) return fail(FPX_ERR_SHAPE_MISMATCH, "ldc %u < rows %u", ldc, rows_p);
+    if (n == 0) return FPX_OK;
+    if (world > 1 && nccl_comm == nullptr) return fail(FPX_ERR_INVALID_VALUE, "world > 1 needs an NCCL communicator");
+    nccl_allgather_fn ag = world > 1 ? nccl_allgather() : nullptr;
+    if (world > 1 && ag == nullptr) return fail(FPX_ERR_DEVICE, "ncclAllGather not found (load NCCL first)");
+    // the FULL problem's split: shard rows are bit-identical to a 1-GPU run
+    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
+    const size_t need = fpx_linear_sharded_workspace_size(rows_p, cols_p, k_act, n, world, split_k);
+    if (workspace == nullptr || workspace_bytes < need)
+        return fail(FPX_ERR_INVALID_VALUE, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
+    uint32_t tr0 = 0, tr1 = 0;
+    fpx_shard_rows(rows_p, rank, world, &tr0, &tr1);
+    const uint32_t slot = shard_slot_rows(rows_p, world), m_local = (tr1 - tr0) * 64u;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
+    float* local = reinterpret_cast<float*>(ws + lin);
+    float* gathered = reinterpret_cast<float*>(ws + lin + align256(size_t(slot) * n * 4));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (m_local > 0) {
+        const int st = fpx_linear(shard_streams, nseg, shard_scales, m_local, cols_p, e, m, act, k_act, n, local, slot,
+                                  split_k, ws, lin, stream);
+        if (st != FPX_OK) return st;
+    }
+    if (nccl_comm == nullptr) {  // world == 1 without a communicator: the slice is all of C
+        FPX_CUDA(launch_gather_shards(local, rows_p, 1, slot, n, c, ldc, s));
+        return FPX_OK;
+    }
+    if (ag == nullptr && (ag = nccl_allgather()) == nullptr)
+        return fail(FPX_ERR_DEVICE, "ncclAllGather not found (load NCCL first)");
+    const int nst = ag(local, gathered, size_t(slot) * n, /*ncclFloat32*/ 7, nccl_comm, s);
+    if (nst != 0) return fail(FPX_ERR_CUDA, "ncclAllGather failed (ncclResult %d)", nst);
+    FPX_CUDA(launch_gather_shards(gathered, rows_p, world, slot, n, c, ldc, s));
     return FPX_OK;
 }
 

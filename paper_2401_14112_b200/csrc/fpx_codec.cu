@@ -434,7 +434,30 @@ __global__ void gather_permute_kernel(const float* __restrict__ g, const uint32_
     }
 }
 
+// gathered [world][n][m_slot] -> col-major C, with each rank's tile-row range
+// recomputed from fpx_shard_rows' formula (no host-side tables).
+__global__ void gather_shards_kernel(const float* __restrict__ g, uint32_t rows_p, int world, uint32_t m_slot,
+                                     uint32_t n, float* __restrict__ c, uint32_t ldc) {
+    const uint64_t trs = rows_p / 64u;
+    const size_t total = static_cast<size_t>(world) * n * m_slot;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint32_t m = static_cast<uint32_t>(i % m_slot);
+        const size_t rest = i / m_slot;
+        const uint32_t j = static_cast<uint32_t>(rest % n);
+        const int r = static_cast<int>(rest / n);
+        const uint32_t tr0 = static_cast<uint32_t>(trs * r / world), tr1 = static_cast<uint32_t>(trs * (r + 1) / world);
+        if (m < (tr1 - tr0) * 64u) c[static_cast<size_t>(j) * ldc + tr0 * 64u + m] = g[i];
+    }
+}
+
 }  // namespace fpxk
+
+cudaError_t launch_gather_shards(const float* g, uint32_t rows_p, int world, uint32_t m_slot, uint32_t n, float* c,
+                                 uint32_t ldc, cudaStream_t st) {
+    fpxk::gather_shards_kernel<<<592, 256, 0, st>>>(g, rows_p, world, m_slot, n, c, ldc);
+    return cudaGetLastError();
+}
 
 // ------------------------------------------------------------ launchers
 using namespace fpxk;

@@ -25,6 +25,8 @@ cudaError_t launch_check_scales(const uint16_t* scales, uint32_t n, int rebias, 
                                 cudaStream_t st);
 cudaError_t launch_stage_act(const uint16_t* src, uint32_t k_act, uint32_t n, uint32_t k_pad, uint16_t* dst,
                              cudaStream_t st);
+cudaError_t launch_gather_shards(const float* g, uint32_t rows_p, int world, uint32_t m_slot, uint32_t n, float* c,
+                                 uint32_t ldc, cudaStream_t st);
 cudaError_t launch_gather_permute(const float* g, const uint32_t* row0, const uint32_t* nrows, int world,
                                   uint32_t m_slot, uint32_t n, float* c, uint32_t ldc, cudaStream_t st);
 

@@ -470,3 +470,43 @@ def test_quantize_pack_fused_errors_and_size(cuda):
     one = fpx.quantize_pack(w, fpx.FpxFormat.e3m2())
     two = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
     assert torch.equal(one.scales, two.scales) and all(torch.equal(a, b) for a, b in zip(one.streams, two.streams))
+
+
+# ------------------------------------------------------------ C-ABI sharded linear (NCCL)
+def test_linear_sharded_c_abi_world1(cuda):
+    """fpx_linear_sharded on one GPU: without a communicator, and through a
+    1-rank NCCL communicator (ncclAllGather resolved from the process at run
+    time) -- both bit-identical to fpx_linear with the same split."""
+    import ctypes as C
+    fpx = _fpx()
+    L = fpx._lib.load()
+    rng = np.random.default_rng(4)
+    w = torch.from_numpy((rng.standard_normal((700, 1024)) * 0.02).astype(np.float32)).to(cuda)
+    p = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
+    nccl = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+
+    class UID(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+
+    uid = UID()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        for n in (1, 16, 40):
+            x = torch.from_numpy(rng.standard_normal((n, 1024)).astype(np.float16)).to(cuda)
+            ref = fpx.gemm_packed(p, x)
+            split = fpx.default_split(p.rows, p.cols, n)
+            ws_n = L.fpx_linear_sharded_workspace_size(p.rows, p.cols, 1024, n, 1, 0)
+            ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
+            ptrs = (C.c_void_p * 2)(*[s.data_ptr() for s in p.streams])
+            for cm in (None, comm):
+                out = torch.full((n, p.rows), float("nan"), device=cuda)
+                st = L.fpx_linear_sharded(ptrs, 2, p.scales.data_ptr(), p.rows, p.cols, 3, 2, x.data_ptr(), 1024, n,
+                                          out.data_ptr(), p.rows, split, 0, 1, cm, ws.data_ptr(), ws_n,
+                                          torch.cuda.current_stream().cuda_stream)
+                assert st == 0, L.fpx_last_error()
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref), (n, cm)
+    finally:
+        nccl.ncclCommDestroy(comm)
