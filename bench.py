@@ -270,40 +270,43 @@ def run_ours(args, rank, world, local):
         s_d2h = torch.cuda.Stream(dev)
 
         def e2e_steps():
-            """Per launch: H2D of its activations on a copy stream, the fused
-            linear on the compute stream, D2H of its C on a second copy stream
-            (PCIe is full duplex).  Events order each launch after its own
-            upload and each download after its own launch, so launch i overlaps
-            the upload of i+1 and the download of i-1: a pipelined decode
-            loop, every byte still crossing PCIe inside the timed region."""
+            """Per step: the step's activations H2D on a copy stream, the six
+            fused linears back to back on the compute stream (consecutive
+            launches keep their programmatic-dependent-launch overlap), the
+            six fp32 C D2H on a second copy stream (PCIe is full duplex).
+            Two buffer sets alternate by step parity, so step k's uploads
+            overlap step k-1's launches and step k-1's downloads overlap step
+            k's: a pipelined decode loop, every byte still crossing PCIe
+            inside the timed region."""
             main = torch.cuda.current_stream(dev)
             c = state["cnt"]
             fork = torch.cuda.Event()
             fork.record(main)
             s_h2d.wait_event(fork)
             s_d2h.wait_event(fork)
-            last_use = {}  # (parity, n) -> event after the D2H that last read d_out / kernel that read d_act
+            ran_ev, down_ev = {}, {}
             for k in range(args.steps):
                 par = k & 1
-                for n in batches:
-                    if (par, n) in last_use:
-                        s_h2d.wait_event(last_use[(par, n)][0])  # d_act[par][n] no longer read
-                        main.wait_event(last_use[(par, n)][1])   # d_out[par][n] already downloaded
-                    with torch.cuda.stream(s_h2d):
+                if k >= 2:
+                    s_h2d.wait_event(ran_ev[k - 2])   # d_act[par] no longer read
+                    main.wait_event(down_ev[k - 2])   # d_out[par] already downloaded
+                with torch.cuda.stream(s_h2d):
+                    for n in batches:
                         d_act[par][n].copy_(h_act[n], non_blocking=True)
-                        up = torch.cuda.Event()
-                        up.record(s_h2d)
-                    main.wait_event(up)
+                    up = torch.cuda.Event()
+                    up.record(s_h2d)
+                main.wait_event(up)
+                for n in batches:
                     launch(c, n, d_act[par][n].data_ptr(), d_out[par][n].data_ptr())
-                    ran = torch.cuda.Event()
-                    ran.record(main)
-                    s_d2h.wait_event(ran)
-                    with torch.cuda.stream(s_d2h):
-                        h_out[n].copy_(d_out[par][n], non_blocking=True)
-                        down = torch.cuda.Event()
-                        down.record(s_d2h)
-                    last_use[(par, n)] = (ran, down)
                     c += 1
+                ran_ev[k] = torch.cuda.Event()
+                ran_ev[k].record(main)
+                s_d2h.wait_event(ran_ev[k])
+                with torch.cuda.stream(s_d2h):
+                    for n in batches:
+                        h_out[n].copy_(d_out[par][n], non_blocking=True)
+                    down_ev[k] = torch.cuda.Event()
+                    down_ev[k].record(s_d2h)
             j1, j2 = torch.cuda.Event(), torch.cuda.Event()
             j1.record(s_h2d)
             j2.record(s_d2h)
@@ -317,9 +320,9 @@ def run_ours(args, rank, world, local):
         e2e = {"value": round(world * nl * WEIGHT_BYTES / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(e2e_ms / args.steps, 4),
-               "note": "per launch: pinned host activations H2D (copy stream) + fpx_linear (C-ABI, compute stream) + "
-                       "fp32 C D2H (second copy stream), pipelined across launches and replayed as one CUDA graph; "
-                       "packed weights resident in HBM"}
+               "note": "per step: pinned host activations H2D (copy stream) + the six fpx_linear calls (C-ABI, "
+                       "compute stream) + fp32 C D2H (second copy stream), double-buffered so copies overlap the "
+                       "neighbouring steps' launches; replayed as one CUDA graph; packed weights resident in HBM"}
 
     # ---- correctness spot check (untimed): last outputs vs a dequant+matmul
     W16 = fpx.dequantize(copies[0]).float()
