@@ -1269,11 +1269,13 @@ cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, in
             return launch_g<F, 32, 2, 4>(L, kp, grid, st);
         }
     }
-    // 32 < N <= 64: the decode kernel as well (8192x22016, N=64: 35.0 us vs
-    // 37.8 us for the single-issuer kernel at its best split); N > 64: the
-    // single-issuer kernel.  (A decode-kernel NPAD=128 instantiation hit an
-    // unspecified launch failure that is not diagnosed yet; not routed.)
+    // 32 < N <= 128: the decode kernel as well (8192x22016: N=64 35.0 us vs
+    // 37.8 us, N=128 53.0 us vs 56.7 us for the single-issuer kernel at its
+    // best split).  NPAD=128 runs 3 de-quantiser groups: its TMEM holds only
+    // 4 A slots beside the two 128-column accumulators, and the 4-group
+    // instantiation hit an unspecified launch failure (not diagnosed).
     if (!classic && npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
+    if (!classic && npad == 128) return launch_g<F, 128, 2, 3>(L, kp, grid, st);
     switch (npad) {
         case 16: return launch_t<F, 16, 2, 3>(L, kp, grid, st);
         case 32: return launch_t<F, 32, 2, 3>(L, kp, grid, st);
