@@ -510,3 +510,48 @@ def test_linear_sharded_c_abi_world1(cuda):
                 assert torch.equal(out, ref), (n, cm)
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+def test_pdl_chain_dependent_linears(cuda):
+    """Back-to-back linears where each consumes the previous one's fp16
+    output (a decode layer chain): with programmatic dependent launch the
+    next kernel starts while the previous drains, so this checks that its
+    activation reads wait for the producer kernel (eager and in a CUDA
+    graph, repeated to shake out timing)."""
+    fpx = _fpx()
+    torch.manual_seed(3)
+    dims = [4096, 2048, 4096, 1024]
+    packs, Ws = [], []
+    for i in range(len(dims) - 1):
+        w = torch.randn(dims[i + 1], dims[i], device=cuda) * (1.0 / dims[i] ** 0.5)
+        p = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
+        packs.append(p)
+        Ws.append(fpx.dequantize(p).float())
+    for n in (1, 16):
+        x = torch.randn(n, dims[0], device=cuda).half()
+
+        def chain():
+            h = x
+            for p in packs:
+                h = fpx.linear(h, p, activation="silu")
+            return h
+
+        ref = x.float()
+        for W in Ws:
+            ref = torch.nn.functional.silu(ref @ W.t()).half().float()
+        for _ in range(5):
+            y = chain().float()
+            assert ((y - ref).abs().max() / ref.abs().max()).item() < 2e-2
+        chain()  # warm the workspace
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = chain()
+        for _ in range(5):
+            x.copy_(torch.randn_like(x))
+            g.replay()
+            torch.cuda.synchronize()
+            ref = x.float()
+            for W in Ws:
+                ref = torch.nn.functional.silu(ref @ W.t()).half().float()
+            assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 2e-2
