@@ -75,6 +75,21 @@ def test_effective_scale_exhaustive(oracle, e, m):
             assert a == b, (e, m, hex(s))
 
 
+def test_default_split_matches_measured_best():
+    """fpx_linear_default_split (waves x (k-tiles per unit + ~10 k-tile
+    per-unit overhead)) picks the split measured fastest on B200 for SURVEY
+    §8d's shapes (profiles/r03/configs_split_sweep.md, bench_configs.py
+    --sweep-splits), and depends on (rows, cols, n) only -- the property the
+    sharded path's bit-identity rests on."""
+    L = _lib.load()
+    expect = {(4096, 4096, 8): 4, (8192, 22016, 1): 2, (8192, 22016, 32): 2, (22016, 8192, 16): 4,
+              (10240, 8192, 16): 3, (8192, 8192, 16): 2, (28672, 8192, 16): 3, (8192, 28672, 16): 2,
+              (8192, 22016, 128): 2}
+    for (m, k, n), s in expect.items():
+        assert L.fpx_linear_default_split(m, k, n) == s, (m, k, n)
+        assert L.fpx_linear_default_split(m, k, n) == L.fpx_linear_default_split(m, k, n)
+
+
 def test_sizes_and_shards():
     L = _lib.load()
     assert L.fpx_pad64(1) == 64 and L.fpx_pad64(64) == 64 and L.fpx_pad64(65) == 128
