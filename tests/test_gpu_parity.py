@@ -555,3 +555,33 @@ def test_pdl_chain_dependent_linears(cuda):
             for W in Ws:
                 ref = torch.nn.functional.silu(ref @ W.t()).half().float()
             assert ((out.float() - ref).abs().max() / ref.abs().max()).item() < 2e-2
+
+
+@pytest.mark.parametrize("n", [1, 16, 32, 64, 128])
+def test_pdl_back_to_back_stress(cuda, n):
+    """Every routed decode-kernel shape, 60 back-to-back launches inside a CUDA
+    graph (programmatic dependent launch mode 2: weights streamed before the
+    dependency wait) over three rotated weight copies; every output checked.
+    Guards the launch-overlap path (two non-routed ring shapes fault only
+    under it -- DESIGN.md §7)."""
+    fpx = _fpx()
+    torch.manual_seed(n)
+    w = torch.randn(4096, 8192, device=cuda) * 0.02
+    p0 = fpx.pack(fpx.quantize_matrix(w, fpx.FpxFormat.e3m2()))
+    copies = [p0] + [fpx.PackedWeights(p0.format, p0.split, p0.rows, p0.cols, p0.orig_rows, p0.orig_cols,
+                                       [s.clone() for s in p0.streams], p0.scales.clone()) for _ in range(2)]
+    x = torch.randn(n, 8192, device=cuda).half()
+    outs = [torch.empty(n, p0.rows, device=cuda) for _ in range(3)]
+    ref = fpx.gemm_packed(p0, x)
+    for i in range(3):
+        fpx.gemm_packed(copies[i], x, out=outs[i])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(60):
+            fpx.gemm_packed(copies[i % 3], x, out=outs[i % 3])
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
