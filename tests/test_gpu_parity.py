@@ -379,7 +379,7 @@ def test_cli_pack_unpack_gemm_check_selftest(cuda, oracle, tmp_path):
 
 
 # ------------------------------------------------------------ fused epilogue (fpx_linear_ex)
-@pytest.mark.parametrize("n", [1, 16, 48, 100])
+@pytest.mark.parametrize("n", [1, 16, 48, 100, 300])
 @pytest.mark.parametrize("split", [0, 1, 3])
 def test_linear_fused_epilogue(cuda, n, split):
     fpx = _fpx()
