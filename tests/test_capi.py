@@ -136,6 +136,31 @@ def test_linear_argument_validation():
     assert L.fpx_linear(ptrs, 2, p, 64, 64, 3, 2, p, 64, 1, p, 32, 1, p, 16, None) == 5  # ldc < rows
 
 
+def test_extended_entry_points_argument_validation():
+    """fpx_linear_ex / fpx_quantize_pack / fpx_linear_sharded reject bad
+    arguments with the reference's error codes before touching a device."""
+    L = _lib.load()
+    buf = (C.c_uint8 * 16)()
+    p = C.cast(buf, C.c_void_p)
+    ptrs = (C.c_void_p * 2)(p, p)
+    bad_dtype = _lib.Epilogue(7, None, 0, None)
+    assert L.fpx_linear_ex(ptrs, 2, p, 64, 64, 3, 2, p, 64, 1, p, 64, 1, C.byref(bad_dtype), p, 16, None) == 3
+    assert b"out_dtype" in L.fpx_last_error()
+    bad_act = _lib.Epilogue(1, None, 9, None)
+    assert L.fpx_linear_ex(ptrs, 2, p, 64, 64, 3, 2, p, 64, 1, p, 64, 1, C.byref(bad_act), p, 16, None) == 3
+    assert L.fpx_linear_ex(ptrs, 2, p, 64, 64, 4, 3, p, 64, 1, p, 64, 1, None, p, 16, None) == 7  # e4m3
+    w3 = (C.c_int * 2)(3, 3)
+    assert L.fpx_quantize_pack(p, 0, 64, 64, 3, 2, w3, 2, ptrs, p, None, None) == 7  # widths 3+3
+    assert L.fpx_quantize_pack(p, 0, 0, 64, 3, 2, None, 0, ptrs, p, None, None) == 5  # empty
+    assert L.fpx_quantize_pack(None, 0, 64, 64, 3, 2, None, 0, ptrs, p, None, None) == 3  # null
+    assert L.fpx_linear_sharded(ptrs, 2, p, 128, 64, 3, 2, p, 64, 1, p, 128, 0, 2, 2, None, p, 16, None) == 3
+    assert L.fpx_linear_sharded(ptrs, 2, p, 128, 64, 3, 2, p, 64, 1, p, 128, 0, 0, 2, None, p, 16, None) == 3
+    assert b"NCCL communicator" in L.fpx_last_error()
+    ws1 = L.fpx_linear_sharded_workspace_size(8192, 22016, 22016, 16, 1, 0)
+    ws8 = L.fpx_linear_sharded_workspace_size(8192, 22016, 22016, 16, 8, 0)
+    assert ws8 > 0 and ws1 > 0
+
+
 def test_python_mirror_api():
     f = fpx.FpxFormat.parse("e3m2")
     assert f == fpx.FpxFormat.e3m2() and f.bias == 3 and f.max_representable() == 28.0
