@@ -591,7 +591,7 @@ struct GCfg {
     // The activation ring only has to outlast a commit batch; everything else
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
-    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 4 : 3);
+    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 6 : 4);
     // Weight producer i issues stages i, i+P, ... into slots it alone owns
     // (SW % P == 0), so it only ever waits on the consumption of its own
     // previous use of a slot: no parity aliasing.  Several producers because
@@ -600,7 +600,9 @@ struct GCfg {
     static constexpr int kWStages =
         std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes) / kP * kP;
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
-    static constexpr int kASlots = (kAccCol0 / 32) / kKS;       // TMEM A stage slots
+    // TMEM A stage slots, at most the activation ring's depth (see the SB >= R
+    // assertion below)
+    static constexpr int kASlots = std::min((kAccCol0 / 32) / kKS, kBStages);
 #ifndef FPX_DEC_BS
 #define FPX_DEC_BS 3
 #endif
@@ -611,6 +613,13 @@ struct GCfg {
     static constexpr uint32_t kWTx = 2 * kKS * (kHiBytes + kLoBytes);
     static constexpr uint32_t kBTx = kKS * kBBytes;
     static_assert(kBStages >= kBS + 1 && kASlots >= kBS + 1 && kWStages >= kG + 1, "ring depths");
+    // A de-quantiser group waits bfull for stage si with a parity wait.  That
+    // is only unambiguous if the activation producer has already issued stage
+    // si - SB into the same slot; it has issued at least stage si - R (the
+    // MMA consumed it, which freed this group's A slot).  Hence SB >= R.
+    // (SB < R let a group pass the wait on the slot's older phase: wrong
+    // results with SB=6, faults with smaller rings.)
+    static_assert(kBStages >= kASlots, "activation ring must be at least as deep as the A-slot ring");
     static_assert(kWStages % kP == 0, "each weight slot is owned by one producer warp");
     static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
