@@ -138,11 +138,11 @@ int fpx_dequantize(const uint8_t* const* streams, int nseg, const int* widths,
  * size is 0.
  * Launch overlap (n <= 32): the kernel uses programmatic dependent launch,
  * so it starts while the preceding kernel in the stream drains.  With
- * FPX_LINEAR_PDL unset or 2 it already streams the packed weights then --
- * they must not be written by a preceding kernel that triggers dependents
- * early (griddepcontrol.launch_dependents); weights are static in
- * inference.  Scales, activations, C and the workspace are only touched
- * after the preceding kernel completed.  FPX_LINEAR_PDL=1 defers every
+ * FPX_LINEAR_PDL unset or 2 it already streams (and de-quantises) the packed
+ * weights and row scales then -- they must not be written by a preceding
+ * kernel that triggers dependents early (griddepcontrol.launch_dependents);
+ * weights are static in inference.  Activations, C and the workspace are
+ * only touched after the preceding kernel completed.  FPX_LINEAR_PDL=1 defers every
  * global access until then; 0 disables the overlap. */
 int fpx_linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n);
 size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int split_k);

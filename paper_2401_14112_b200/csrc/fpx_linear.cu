@@ -1025,11 +1025,12 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     raw[lc][hf] = tr_ < p.tile_rows ? __ldg(&p.scales[tr_ * 64 + 16 * (2 * h + lc) + 8 * hf + lane / 4])
                                                     : uint16_t(0);
         };
-        // Even in PDL mode 2 the de-quantisers start only once the preceding
-        // grid has completed: letting them run ahead (LDS, math, TMEM stores,
-        // scale loads) was worth <= 1 us and two ring shapes faulted under it
-        // (DESIGN.md §7); the weight ring is still filled early by the producer.
-        grid_dep_wait();
+        // PDL mode 2: the row scales are immutable like the weights, so the
+        // groups de-quantise their first stages while the preceding kernel
+        // drains; they block on bfull until the activations (loaded after
+        // griddepcontrol.wait) land.  That wait is unambiguous because SB >= R
+        // (GCfg); with SB < R it aliased and this early start exposed it.
+        if (p.pdl != 2u) grid_dep_wait();
         uint16_t nxt[2][2] = {{0, 0}, {0, 0}};
         if (u_begin < u_end) fetch_scales(u_begin, nxt);
         uint32_t si = 0;
@@ -1137,12 +1138,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Programmatic dependent launch (FPX_LINEAR_PDL, read once):
 //   2 (default) the kernel may start while the preceding kernel in the stream
-//     drains: prologue, TMEM allocation and the weight ring's first pass
-//     (TMA) begin at once; everything else -- de-quantisation, row scales,
-//     activations, C, partials, counters -- waits for griddepcontrol.wait.
-//     Requires that the packed weight streams are not written by a preceding
-//     kernel that triggers dependents early (inference: weights are static).
-//     Measured ~3 us per launch.
+//     drains: prologue, TMEM allocation, the weight ring's first pass and the
+//     de-quantisation of the first stages (weights + row scales) begin at
+//     once; activations, C, partials and counters wait for
+//     griddepcontrol.wait.  Requires that the packed weights and scales are
+//     not written by a preceding kernel that triggers dependents early
+//     (inference: weights are static).  Measured ~3 us per launch.
 //   1 PDL with every global access after griddepcontrol.wait (hides the
 //     launch latency and prologue only, ~1.2 us).
 //   0 plain stream order.
