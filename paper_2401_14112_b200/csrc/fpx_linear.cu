@@ -585,13 +585,19 @@ struct GCfg {
 #ifndef FPX_DEC_SB
 #define FPX_DEC_SB 8
 #endif
+#ifndef FPX_DEC_SB64
+#define FPX_DEC_SB64 6
+#endif
+#ifndef FPX_DEC_SB128
+#define FPX_DEC_SB128 4
+#endif
 #ifndef FPX_DEC_SMEM_KB
 #define FPX_DEC_SMEM_KB 216
 #endif
     // The activation ring only has to outlast a commit batch; everything else
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
-    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? 6 : 4);
+    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? FPX_DEC_SB64 : FPX_DEC_SB128);
     // Weight producer i issues stages i, i+P, ... into slots it alone owns
     // (SW % P == 0), so it only ever waits on the consumption of its own
     // previous use of a slot: no parity aliasing.  Several producers because
@@ -850,6 +856,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         uint32_t as = 0, aph = 0;   // A slot and its phase parity
         uint32_t bsl = 0;           // activation slot
         uint32_t nb = 0, nbs = 0;   // stages in the open commit batch, batch barrier slot
+        uint32_t nbatch = 0;        // batch commits issued
         for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
             uint32_t mt, ch, s0, ns;
             unit_stages<KS>(p, u, mt, ch, s0, ns);
@@ -877,6 +884,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 }
                 if (++nb == static_cast<uint32_t>(BS)) {
                     umma_commit_warp(&done[nbs]);
+                    ++nbatch;
                     nb = 0;
                     nbs = (nbs + 1 == static_cast<uint32_t>(NB)) ? 0u : nbs + 1;
                 }
@@ -886,7 +894,16 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             }
             umma_commit_warp(&accfull[ab]);
         }
-        if (nb != 0) umma_commit_warp(&done[nbs]);  // final partial batch
+        if (nb != 0) umma_commit_warp(&done[nbs]), ++nbatch;  // final partial batch
+        // The last batch commits have no consumer (no later stage reuses
+        // their slots) and the final partial one is even issued after the
+        // last accfull commit: wait for the newest so that no tcgen05.commit
+        // arrival can land in this CTA's shared memory after it exits -- i.e.
+        // in the barriers of the next CTA placed on this SM.
+        if (nbatch != 0) {
+            const uint32_t b = nbatch - 1;
+            mbar_wait(&done[b % NB], (b / NB) & 1u);
+        }
     } else if (warp >= C::kEpiWarp0) {
         // ------------------------------------------------ epilogue
         grid_dep_wait();  // C / partials / counters may still be in use by the preceding kernel
