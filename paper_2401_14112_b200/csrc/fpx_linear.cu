@@ -606,9 +606,10 @@ struct GCfg {
     static constexpr int kWStages =
         std::min(24, (FPX_DEC_SMEM_KB * 1024 - 2048 - kBStages * kBStageBytes) / kWStageBytes) / kP * kP;
     static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
-    // TMEM A stage slots, at most the activation ring's depth (see the SB >= R
-    // assertion below)
-    static constexpr int kASlots = std::min((kAccCol0 / 32) / kKS, kBStages);
+    // TMEM A stage slots, at most the activation ring's depth and the weight
+    // ring's depth minus the groups (see the SB >= R and SW >= G + R
+    // assertions below)
+    static constexpr int kASlots = std::min(std::min((kAccCol0 / 32) / kKS, kBStages), kWStages - kG);
 #ifndef FPX_DEC_BS
 #define FPX_DEC_BS 3
 #endif
@@ -626,6 +627,12 @@ struct GCfg {
     // (SB < R let a group pass the wait on the slot's older phase: wrong
     // results with SB=6, faults with smaller rings.)
     static_assert(kBStages >= kASlots, "activation ring must be at least as deep as the A-slot ring");
+    // The same argument for the weight ring: a group waits wfull for stage si
+    // right after finishing its stage si - G, whose A slot required the MMA to
+    // have consumed stage si - G - R -- so every stage up to there has landed.
+    // The slot's previous phase (stage si - SW) must be among them:
+    // SW >= G + R.  (NPAD=64 had SW 9 < 4 + 6.)
+    static_assert(kWStages >= kG + kASlots, "weight ring must cover the groups plus the A-slot ring");
     static_assert(kWStages % kP == 0, "each weight slot is owned by one producer warp");
     static_assert(NPAD <= 128, "double-buffered NPAD-column accumulators + A ring must fit 512 TMEM columns");
 };
