@@ -583,7 +583,7 @@ struct GCfg {
     static constexpr int kWStageBytes = (2 * kKS * (kHiBytes + kLoBytes) + 1023) / 1024 * 1024;
     static constexpr int kBStageBytes = (kKS * kBBytes + 1023) / 1024 * 1024;
 #ifndef FPX_DEC_SB
-#define FPX_DEC_SB 8
+#define FPX_DEC_SB 12
 #endif
 #ifndef FPX_DEC_SB64
 #define FPX_DEC_SB64 6
