@@ -237,6 +237,14 @@ def run_ours(args, rank, world, local):
         for _ in range(args.steps):
             c = step(c)
 
+    # per-batch device time of the fused kernel (informational: graph of 12
+    # launches per N, 3 weight copies rotated), measured before the timed
+    # region and its clock soak
+    per_n = {}
+    for n in batches:
+        gr = capture(lambda: [launch(i, n, acts[n].data_ptr(), outs[n].data_ptr()) for i in range(12)])
+        per_n[n] = max_over_ranks(timed(gr, 2) * 1e3 / 24)  # us per launch
+
     g_steps = capture(k_steps)
     for _ in range(args.warmup):  # warm-up replays of the timed graph itself
         g_steps.replay()
@@ -251,12 +259,6 @@ def run_ours(args, rank, world, local):
             g_steps.replay()
             torch.cuda.synchronize(dev)
 
-    # per-batch device time of the fused kernel (graph of 12 launches, 3 weight copies rotated)
-    per_n = {}
-    for n in batches:
-        gr = capture(lambda: [launch(i, n, acts[n].data_ptr(), outs[n].data_ptr()) for i in range(12)])
-        per_n[n] = max_over_ranks(timed(gr, 2) * 1e3 / 24)  # us per launch
-    mean_launch_us = float(np.mean(list(per_n.values())))
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -349,6 +351,9 @@ def run_ours(args, rank, world, local):
     hbm, hbm_src = peaks()
     traffic, traffic_src = ncu_traffic()
     value = world * nl * WEIGHT_BYTES / (total_ms * 1e-3) / 1e9
+    # the timed region holds only fused-kernel launches (nl of them per rank):
+    # its mean launch duration is the kernel's, measured live on its stream
+    mean_launch_us = total_ms * 1e3 / nl
     achieved = WEIGHT_BYTES / (mean_launch_us * 1e-6) / 1e9
     res = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -365,7 +370,9 @@ def run_ours(args, rank, world, local):
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "traffic_source": f"{traffic_src} (N=16 launch, dram read+write bytes)" if traffic else None,
                      "peak_source": f"{hbm_src} MEASURED_PEAKS.json hbm_gbs" if hbm_src == "measured" else hbm_src,
-                     "kernel": "fpx_linear_decode_kernel (mean device time per launch over the batch sweep)",
+                     "kernel": "fpx_linear_decode_kernel (mean device time per launch over the timed region: "
+                               "K steps x the batch sweep, back to back)",
+                     "us_per_launch": round(mean_launch_us, 2),
                      "algorithmic_bytes_per_launch": WEIGHT_BYTES},
         "gpu_launches": nl,  # one fused kernel per batch per step
         "clocks": clk.summary(),
