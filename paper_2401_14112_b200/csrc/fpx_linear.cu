@@ -585,6 +585,9 @@ struct GCfg {
 #ifndef FPX_DEC_SB
 #define FPX_DEC_SB 12
 #endif
+#ifndef FPX_DEC_SB32
+#define FPX_DEC_SB32 FPX_DEC_SB
+#endif
 #ifndef FPX_DEC_SB64
 #define FPX_DEC_SB64 6
 #endif
@@ -597,7 +600,8 @@ struct GCfg {
     // The activation ring only has to outlast a commit batch; everything else
     // goes to the weight ring, whose depth (bytes in flight per SM) sets the
     // sustainable HBM rate against the ~2.5 us loaded TMA latency.
-    static constexpr int kBStages = NPAD <= 32 ? FPX_DEC_SB : (NPAD == 64 ? FPX_DEC_SB64 : FPX_DEC_SB128);
+    static constexpr int kBStages =
+        NPAD <= 16 ? FPX_DEC_SB : (NPAD == 32 ? FPX_DEC_SB32 : (NPAD == 64 ? FPX_DEC_SB64 : FPX_DEC_SB128));
     // Weight producer i issues stages i, i+P, ... into slots it alone owns
     // (SW % P == 0), so it only ever waits on the consumption of its own
     // previous use of a slot: no parity aliasing.  Several producers because
