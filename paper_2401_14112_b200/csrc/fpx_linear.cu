@@ -173,12 +173,20 @@ struct Cfg {
     static constexpr int kStages = std::min(16, kSmemBudget / kStageBytes);
     static constexpr int kAccBufs = NPAD <= 128 ? 2 : 1;
     static constexpr int kACols = 32 * kKS;  // TMEM columns per A stage
-    static constexpr int kAStages = std::min(8, int((kTmemCols - kAccBufs * NPAD) / kACols));
+    // A slots, at most the stage ring's depth minus the groups: a group waits
+    // `full` for stage si right after its stage si - NG, whose A slot proved
+    // the MMA consumed stage si - NG - kAStages; the slot's previous phase
+    // (stage si - kStages) must be among those, else the parity wait aliases
+    // (the decode kernel's race; here it gave the intermittent
+    // NPAD=256 errors).
+    static constexpr int kAStages =
+        std::min(std::min(8, int((kTmemCols - kAccBufs * NPAD) / kACols)), kStages - kNG);
     static constexpr int kAccCol0 = kAStages * kACols;
     static constexpr int kBarBytes = 8 * (2 * kStages + 2 * kAStages + 4) + 16;
     static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
     static_assert(kStages >= 2, "smem stages");
     static_assert(kAStages >= kNG + 1, "tmem A stages");
+    static_assert(kStages >= kNG + kAStages, "stage ring must cover the groups plus the A-slot ring");
     static_assert(kAccCol0 + kAccBufs * NPAD <= int(kTmemCols), "tmem budget");
 };
 
@@ -1151,6 +1159,9 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     if (p.split > 1) final_split_reduce<NPAD>(p, final_red, C::kThreads);
 }
 
+#ifndef FPX_CLASSIC_CAP
+#define FPX_CLASSIC_CAP 0
+#endif
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1241,12 +1252,12 @@ cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
     auto kern = fpx_linear_kernel<F, NPAD, KS_, NG_>;
     CUtensorMap map;
     if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
-    // NPAD = 256 (single accumulator buffer): intermittent wrong results were
-    // measured at split 9 (not understood yet); split is capped at 2 -- the
-    // default for this width -- and each CTA runs one unit.  The cap depends
-    // on N only, so tile-row shards still reproduce the unsharded rows.
+    // NPAD = 256 (single accumulator buffer): the intermittent wrong results
+    // once measured at split 9 were the stage-ring parity aliasing now ruled
+    // out by Cfg (kStages >= NG + kAStages); FPX_CLASSIC_CAP=1 restores the
+    // old cap at split 2 (the default split for this width anyway).
     KParams kq = kp;
-    if (C::kAccBufs == 1 && kq.split > 2) {
+    if (FPX_CLASSIC_CAP && C::kAccBufs == 1 && kq.split > 2) {
         kq.split = 2;
         kq.units = (kp.rows_p + kTileM - 1) / kTileM * 2;
     }
@@ -1314,18 +1325,13 @@ cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, in
     }
     // 32 < N <= 128: the decode kernel as well (8192x22016: N=64 35.0 us vs
     // 37.8 us, N=128 53.0 us vs 56.7 us for the single-issuer kernel at its
-    // best split).  NPAD=128 runs 3 de-quantiser groups: its TMEM holds only
-    // 4 A slots beside the two 128-column accumulators, and the 4-group
-    // instantiation hit an unspecified launch failure (not diagnosed).
-    if (!classic && npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
-    if (!classic && npad == 128) return launch_g<F, 128, 2, 3>(L, kp, grid, st);
-    switch (npad) {
-        case 16: return launch_t<F, 16, 2, 3>(L, kp, grid, st);
-        case 32: return launch_t<F, 32, 2, 3>(L, kp, grid, st);
-        case 64: return launch_t<F, 64, 2, 3>(L, kp, grid, st);
-        case 128: return launch_t<F, 128, 2, 2>(L, kp, grid, st);
-        case 256: return launch_t<F, 256, 1, 3>(L, kp, grid, st);
-    }
+    // best split).  NPAD=128 runs 3 de-quantiser groups (4 measured equal).
+    if (npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
+    if (npad == 128) return launch_g<F, 128, 2, 3>(L, kp, grid, st);
+    (void)classic;  // N <= 128 always runs the decode kernel
+    if (npad <= 16) return launch_g<F, 16, 2, 4>(L, kp, grid, st);
+    if (npad == 32) return launch_g<F, 32, 2, 4>(L, kp, grid, st);
+    if (npad == 256) return launch_t<F, 256, 1, 2>(L, kp, grid, st);
     return cudaErrorInvalidValue;
 }
 
