@@ -13,14 +13,23 @@
 //   FpxFormat / SplitScheme          format.hpp:16-59
 //   ErrorCode / Error                error.hpp:10-44
 //   Dtype / Layout / ScalarMatrix    codec.hpp:10-30
+//   half_to_float / float_to_half / half_mul / half_is_finite / half_is_nan
+//                                    half.hpp:9-21 (host scalar helpers)
 //   QuantizedMatrix                  codec.hpp:37-51
-//   quantize_matrix / effective_scale codec.hpp:66,76 (dequantize_reference
-//                                    stays a reference-only oracle; its device
-//                                    equivalent here is fpx::dequantize)
+//   decode_scalar / encode_scalar    codec.hpp:56,60 (host scalar codec)
+//   quantize_matrix / effective_scale codec.hpp:66,76
+//   dequantize_reference             codec.hpp:72 (on the device, bit-exact)
 //   PackedWeights / pack / unpack    prepack.hpp:64-86
 //   gemm_packed                      gemm.hpp:27-28 (trace pointer: the
 //                                    bank-conflict trace is a CPU-simulator
 //                                    artefact; a non-null trace is rejected)
+//   gemm_reference                   gemm.hpp:32: pack + the same fused
+//                                    kernel, so gemm_reference(q, b) ==
+//                                    gemm_packed(pack(q), b) bit for bit -- the
+//                                    reference's own contract (gemm.hpp:30-31)
+//   io.hpp:13-41                     MatrixFile / PackFile containers
+// Reference-style includes ("fpx/codec.hpp", "fpx/gemm.hpp", ...) resolve to
+// this header through include/fpx/*.hpp.
 #pragma once
 
 #include <cstddef>
@@ -85,6 +94,8 @@ struct FpxFormat {
     uint32_t code_mask() const { return code_count() - 1; }
     uint32_t sign_mask() const { return 1u << (exp_bits + man_bits); }
     float max_representable() const;
+    // Code spacing at |x|: 2^(e-M), e = floor(log2|x|) clamped to [1-bias, emax].
+    float ulp_at(double magnitude) const;
     std::string name() const;
     bool operator==(const FpxFormat&) const = default;
 
@@ -104,6 +115,13 @@ struct SplitScheme {
     static SplitScheme for_format(const FpxFormat& fmt);
     static SplitScheme make(std::vector<int> widths, const FpxFormat& fmt);
 };
+
+// ------------------------------------------------------------------ half.hpp
+float half_to_float(uint16_t h);
+uint16_t float_to_half(float f);          // RNE, subnormals kept, overflow -> inf
+uint16_t half_mul(uint16_t a, uint16_t b);  // fp32 product (exact) rounded RNE to fp16
+constexpr bool half_is_finite(uint16_t h) { return (h & 0x7c00u) != 0x7c00u; }
+constexpr bool half_is_nan(uint16_t h) { return (h & 0x7c00u) == 0x7c00u && (h & 0x03ffu) != 0; }
 
 // ------------------------------------------------------------------ matrices
 enum class Dtype : uint32_t { Fp32 = 0, Fp16 = 1 };
@@ -136,6 +154,15 @@ struct QuantizedMatrix {
     bool operator==(const QuantizedMatrix&) const = default;
 };
 
+// prepack.hpp:15-21 tiling constants
+inline constexpr uint32_t kTileDim = 64;
+inline constexpr uint32_t kSlicesPerTile = 4;
+inline constexpr uint32_t kChunksPerSlice = 4;
+inline constexpr uint32_t kPairsPerChunk = 4;
+inline constexpr uint32_t kWarpSize = 32;
+inline constexpr uint32_t kCodesPerThread = 128;
+inline constexpr uint32_t kCodesPerThreadSlice = 32;
+
 struct PackedWeights {
     FpxFormat format;
     SplitScheme split;
@@ -156,7 +183,13 @@ struct BankAccessTrace;  // reference simulator type; not supported on the GPU p
 // ------------------------------------------------------------------ API
 ScalarMatrix to_fp32(const ScalarMatrix& m);
 ScalarMatrix to_fp16(const ScalarMatrix& m);
+// Exact value of a code (InvalidCode if it has bits above the format's width).
+float decode_scalar(uint32_t code, const FpxFormat& fmt);
+// Nearest code, ties to even, saturating; InvalidValue on NaN.
+uint32_t encode_scalar(double value, const FpxFormat& fmt);
 QuantizedMatrix quantize_matrix(const ScalarMatrix& m, const FpxFormat& fmt);
+// fp16 row-major padded W = fp16(decode(code)) x scale, fp16 RNE (K3 on the device).
+ScalarMatrix dequantize_reference(const QuantizedMatrix& q);
 uint16_t effective_scale(uint16_t row_scale, const FpxFormat& fmt);
 PackedWeights pack(const QuantizedMatrix& q);
 PackedWeights pack(const QuantizedMatrix& q, const SplitScheme& split);
@@ -166,7 +199,12 @@ QuantizedMatrix unpack(const PackedWeights& p);
 ScalarMatrix dequantize(const PackedWeights& p);
 // C fp32 col-major (padded rows x n) = dequant(A) x B, B fp16 col-major.
 ScalarMatrix gemm_packed(const PackedWeights& a, const ScalarMatrix& b, BankAccessTrace* trace = nullptr);
+// Same C as gemm_packed(pack(q), b), bit for bit (gemm.hpp:30-32).
+ScalarMatrix gemm_reference(const QuantizedMatrix& q, const ScalarMatrix& b);
 
+inline constexpr char kMatrixMagic[8] = {'F', 'P', 'X', 'M', 'A', 'T', '1', 0};
+inline constexpr char kPackMagic[8] = {'F', 'P', 'X', 'P', 'A', 'C', 'K', '1'};
+inline constexpr uint16_t kPackVersion = 1;
 // io.hpp:27-41 -- MatrixFile ("FPXMAT1\0") and PackFile ("FPXPACK1")
 // containers, little-endian, strict validation (Truncated / BadMagic /
 // BadVersion / Corrupt errors carry the byte offset).

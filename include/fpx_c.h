@@ -7,7 +7,10 @@
  *   fpx_quantize      <- quantize_matrix        codec.hpp:66   (codec.cpp:105-177)
  *   fpx_prepack       <- pack                   prepack.hpp:84-85 (prepack.cpp:153-209)
  *   fpx_unpack        <- unpack                 prepack.hpp:86  (prepack.cpp:211-260)
- *   fpx_dequantize    <- dequantize_reference   codec.hpp:72   (codec.cpp:179-193)
+ *   fpx_dequantize    <- dequantize_reference(unpack(p))    (codec.cpp:179-193)
+ *   fpx_dequantize_codes <- dequantize_reference codec.hpp:72   (codec.cpp:179-193)
+ *   fpx_decode_scalar <- decode_scalar          codec.hpp:56   (codec.cpp:49-68)
+ *   fpx_encode_scalar <- encode_scalar          codec.hpp:60   (codec.cpp:70-103)
  *   fpx_linear        <- gemm_packed            gemm.hpp:27-28 (gemm.cpp:170-219)
  *   fpx_effective_scale <- effective_scale      codec.hpp:76   (codec.cpp:195-199)
  *   fpx_format_check / fpx_split_for_format / fpx_max_representable
@@ -28,6 +31,7 @@
  *   - Functions whose reference counterpart throws on data-dependent errors
  *     (NaN row, scale overflow) synchronise `stream` when `status_dev` is
  *     NULL and return the error; pass a device status word to stay async.
+ *   - Workspaces (fpx_linear*): one per stream, see fpx_linear below.
  *   - Formats: exp_bits/man_bits as FpxFormat (E 1..5, M 0..6, 3..8 bits).
  *     The fused linear kernel serves e3m2 and e2m3 ([2,4] split) and e2m2
  *     ([4,1] split); pack/unpack/dequantize/quantize serve every format.
@@ -83,6 +87,11 @@ uint16_t fpx_effective_scale(uint16_t row_scale, int exp_bits, int man_bits);
 uint32_t fpx_pad64(uint32_t n);
 /* Bytes of segment `seg` of a rows_p x cols_p packed matrix (512*w per tile). */
 size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width);
+/* Scalar codec (host): exact value of a code (FPX_ERR_INVALID_CODE if it has
+ * bits above the format's width) / nearest code, ties to even, saturating
+ * (FPX_ERR_INVALID_VALUE for NaN). */
+int fpx_decode_scalar(uint32_t code, int exp_bits, int man_bits, float* value);
+int fpx_encode_scalar(double value, int exp_bits, int man_bits, uint32_t* code);
 
 /* ---- K0: quantize (codec.cpp:105-177) --------------------------------
  * w: rows x cols row-major, dtype FPX_FP32 or FPX_FP16 (device).
@@ -93,6 +102,14 @@ size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width);
  * first failing row, or UINT64_MAX; when NULL the call synchronises. */
 int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int exp_bits, int man_bits,
                  uint8_t* codes, uint16_t* scales, uint64_t* status_dev, fpx_stream_t stream);
+
+/* ---- dequantize_reference from the code matrix (codec.cpp:179-193) -----
+ * w_f16[r][c] = fp16(decode(codes[r][c])) * scales[r] in fp16 RNE, bit-exact,
+ * rows_p x cols_p row-major (codes and w_f16 16-byte aligned).  A code with
+ * bits above the format's width is FPX_ERR_INVALID_CODE (first failing row;
+ * status_dev as in fpx_quantize, NULL = synchronous). */
+int fpx_dequantize_codes(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int exp_bits,
+                         int man_bits, uint16_t* w_f16, uint64_t* status_dev, fpx_stream_t stream);
 
 /* ---- K0+K1 fused: quantize straight into the packed streams
  * Bit-exact with fpx_quantize followed by fpx_prepack (same scales, same
@@ -133,19 +150,27 @@ int fpx_dequantize(const uint8_t* const* streams, int nseg, const int* widths,
  * result depends only on (W, act, split_k) -- never on scheduling -- so a
  * tile-row shard computed with the full problem's split_k is bit-identical
  * to the same rows of the unsharded result.
- * workspace: device buffer of >= fpx_linear_workspace_size(...) bytes,
- * zero-filled once before first use (it self-cleans); may be NULL when the
- * size is 0.
- * Launch overlap (n <= 32): the kernel uses programmatic dependent launch,
- * so it starts while the preceding kernel in the stream drains.  With
- * FPX_LINEAR_PDL unset or 2 it already streams (and de-quantises) the packed
- * weights and row scales then -- they must not be written by a preceding
- * kernel that triggers dependents early (griddepcontrol.launch_dependents);
- * weights are static in inference.  Activations, C and the workspace are
- * only touched after the preceding kernel completed.  FPX_LINEAR_PDL=1 defers every
- * global access until then; 0 disables the overlap. */
+ * workspace: device buffer of >= fpx_linear_workspace_size(...) bytes
+ * (never NULL: it always holds the 64 KiB split-K arrival-counter table),
+ * zero-filled once before first use; the counters self-clean after every
+ * launch.  ONE WORKSPACE PER STREAM: two calls that may run concurrently
+ * (distinct streams) must not share a workspace.  A call whose launch fails
+ * clears the counters itself; fpx_linear_workspace_reset() clears them
+ * explicitly (e.g. after a workspace was reused for other data).
+ * Launch overlap (n <= 128, the decode kernel): the kernel uses programmatic
+ * dependent launch, so it starts while the preceding kernel in the stream
+ * drains.  With FPX_LINEAR_PDL unset or 2 it already streams (and
+ * de-quantises) the packed weights and row scales then -- they must not be
+ * written by a preceding kernel that triggers dependents early
+ * (griddepcontrol.launch_dependents); weights are static in inference.  This
+ * library's own weight writers (fpx_quantize, fpx_quantize_pack,
+ * fpx_prepack) are guarded: the next linear on the same stream defers every
+ * read until they completed.  Activations, C and the workspace are only
+ * touched after the preceding kernel completed.  FPX_LINEAR_PDL=1 defers
+ * every global access until then; 0 disables the overlap. */
 int fpx_linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n);
 size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int split_k);
+int fpx_linear_workspace_reset(void* workspace, size_t workspace_bytes, fpx_stream_t stream);
 int fpx_linear(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
                uint32_t cols_p, int exp_bits, int man_bits, const uint16_t* act, uint32_t k_act, uint32_t n,
                float* c, uint32_t ldc, int split_k, void* workspace, size_t workspace_bytes,

@@ -185,6 +185,8 @@ class Reference:
         L.ref_release.argtypes = [C.c_void_p]
         L.ref_gemm_packed.argtypes = [C.c_void_p, _u16p, C.c_uint32, C.c_uint32, _f32p]
         L.ref_gemm_reference.argtypes = [C.c_void_p, _u16p, C.c_uint32, C.c_uint32, _f32p]
+        L.ref_gemm_reference_codes.argtypes = [_u8p, _u16p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                               C.c_int, _u16p, C.c_uint32, C.c_uint32, _f32p]
 
     def last_error(self) -> str:
         return self.lib.ref_last_error().decode()
@@ -217,6 +219,20 @@ class Reference:
         st = self.lib.ref_dequantize(_p(np.ascontiguousarray(codes), _u8p), _p(np.ascontiguousarray(scales), _u16p),
                                      rp, cp, e, m, _p(out, _u16p))
         return st, out
+
+    def gemm_reference(self, codes, scales, e, m, b_colmajor: np.ndarray, orig_cols=None, orig_rows=None):
+        """gemm.cpp:221-252 on (codes, scales) directly; b_colmajor uint16 [n, b_rows].
+        Returns C as float32 [n, rows_p] (col-major rows_p x n)."""
+        rp, cp = codes.shape
+        b = np.ascontiguousarray(b_colmajor, dtype=np.uint16)
+        n, b_rows = b.shape
+        c = np.zeros((n, rp), np.float32)
+        st = self.lib.ref_gemm_reference_codes(_p(np.ascontiguousarray(codes), _u8p),
+                                               _p(np.ascontiguousarray(scales), _u16p), rp, cp, orig_rows or rp,
+                                               orig_cols or cp, e, m, _p(b, _u16p), b_rows, n, _p(c, _f32p))
+        if st:
+            raise RuntimeError(self.last_error())
+        return c
 
     def prepare(self, codes, scales, e, m, orig_rows=None, orig_cols=None):
         rp, cp = codes.shape

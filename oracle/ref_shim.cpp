@@ -157,6 +157,21 @@ int ref_gemm_packed(void* h, const uint16_t* b, uint32_t b_rows, uint32_t n, flo
     }
 }
 
+// gemm_reference straight from codes (no pack): the parity tests' oracle C
+// for full-size problems.  C: fp32 col-major rows_p x n.
+int ref_gemm_reference_codes(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p,
+                             uint32_t orig_rows, uint32_t orig_cols, int e, int m, const uint16_t* b, uint32_t b_rows,
+                             uint32_t n, float* c) {
+    try {
+        fpx::ScalarMatrix out = fpx::gemm_reference(make_q(codes, scales, rows_p, cols_p, orig_rows, orig_cols, e, m),
+                                                    make_b(b, b_rows, n));
+        std::memcpy(c, out.f32.data(), out.f32.size() * 4);
+        return 0;
+    } catch (const fpx::Error& err) {
+        return fail(err);
+    }
+}
+
 int ref_gemm_reference(void* h, const uint16_t* b, uint32_t b_rows, uint32_t n, float* c) {
     try {
         auto* r = static_cast<RefPrepared*>(h);

@@ -79,6 +79,11 @@ def load(path: str | None = None) -> C.CDLL:
         "fpx_dequantize": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _intp, C.c_void_p, C.c_uint32, C.c_uint32,
                                      C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
         "fpx_linear_default_split": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32]),
+        "fpx_linear_workspace_reset": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
+        "fpx_decode_scalar": (C.c_int, [C.c_uint32, C.c_int, C.c_int, _f32p]),
+        "fpx_encode_scalar": (C.c_int, [C.c_double, C.c_int, C.c_int, _u32p]),
+        "fpx_dequantize_codes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]),
         "fpx_linear_workspace_size": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
         "fpx_linear": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int,
                                  C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int,

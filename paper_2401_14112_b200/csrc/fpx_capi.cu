@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/fpx_c.h"
 #include "fpx_internal.h"
@@ -142,6 +143,35 @@ volatile unsigned long long* debug_progress_buffer() {
     return static_cast<volatile unsigned long long*>(dev);
 }
 
+// PDL guard.  The fused linear's default launch mode streams packed weights
+// and row scales before griddepcontrol.wait (pdl_mode 2, fpx_linear.cu).
+// When one of this library's own kernels has just written packed weights or
+// scales on a stream (quantize, quantize_pack, prepack), the next linear on
+// that stream is capped at mode 1 -- every global read after the wait, i.e.
+// after the writer completed and its stores are visible -- and the mark is
+// cleared.  Writers on other streams reach the linear only through an event
+// wait, which is never a programmatic edge.
+std::mutex g_dirty_mu;
+std::vector<cudaStream_t> g_dirty;
+
+void mark_weights_written(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_dirty_mu);
+    for (cudaStream_t d : g_dirty)
+        if (d == s) return;
+    g_dirty.push_back(s);
+}
+
+bool take_weights_written(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_dirty_mu);
+    for (size_t i = 0; i < g_dirty.size(); ++i)
+        if (g_dirty[i] == s) {
+            g_dirty[i] = g_dirty.back();
+            g_dirty.pop_back();
+            return true;
+        }
+    return false;
+}
+
 }  // namespace
 
 extern "C" {
@@ -213,6 +243,45 @@ uint16_t fpx_effective_scale(uint16_t s, int e, int m) {
 
 uint32_t fpx_pad64(uint32_t n) { return (n + 63u) / 64u * 64u; }
 
+// codec.cpp:49-68: exact value of a code, (-1)^S 1.M 2^(E-bias) or
+// 0.M 2^(1-bias), computed in double and narrowed to float (exact for every
+// format of at most 8 bits).
+int fpx_decode_scalar(uint32_t code, int e, int m, float* out) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (code >= (1u << (1 + e + m)))
+        return fail(FPX_ERR_INVALID_CODE, "code %u out of range for e%dm%d", code, e, m);
+    const uint32_t sign = code >> (e + m), ef = (code >> m) & ((1u << e) - 1u), mf = code & ((1u << m) - 1u);
+    const double v = ef == 0 ? std::ldexp(double(mf), 1 - bias_of(e) - m)
+                             : std::ldexp(double((1u << m) + mf), int(ef) - bias_of(e) - m);
+    const float f = static_cast<float>(v);
+    if (out) *out = sign ? -f : f;
+    return FPX_OK;
+}
+
+// codec.cpp:70-103: nearest code, ties to even, saturating beyond
+// max_representable; NaN is InvalidValue.  The same arithmetic as the
+// quantize kernel's encode (fpx_codec.cu encode_dev).
+int fpx_encode_scalar(double v, int e, int m, uint32_t* out) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (std::isnan(v)) return fail(FPX_ERR_INVALID_VALUE, "cannot encode NaN");
+    const uint32_t smask = 1u << (e + m);
+    const uint32_t sign = std::signbit(v) ? smask : 0u;
+    const double a = std::fabs(v);
+    uint32_t code;
+    if (a > static_cast<double>(fpx_max_representable(e, m))) {
+        code = sign | (smask - 1u);
+    } else {
+        const int emin = 1 - bias_of(e);
+        int ex = a >= std::ldexp(1.0, emin) ? std::ilogb(a) : emin;
+        uint32_t k = static_cast<uint32_t>(std::nearbyint(std::ldexp(a, m - ex)));
+        const uint32_t unit = 1u << m;
+        if (k == 2u * unit) k = unit, ++ex;
+        code = k < unit ? (sign | k) : (sign | (static_cast<uint32_t>(ex + bias_of(e)) << m) | (k - unit));
+    }
+    if (out) *out = code;
+    return FPX_OK;
+}
+
 size_t fpx_stream_bytes(uint32_t rows_p, uint32_t cols_p, int width) {
     return static_cast<size_t>(rows_p / 64u) * (cols_p / 64u) * 512u * static_cast<size_t>(width);
 }
@@ -237,6 +306,7 @@ int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, 
     const double maxrep = static_cast<double>(fpx_max_representable(e, m));
     FPX_CUDA(launch_quantize(w, dtype, rows, cols, fpx_pad64(rows), fpx_pad64(cols), e, m, maxrep, codes, scales,
                              status, s));
+    mark_weights_written(s);
     if (!own) return FPX_OK;
     unsigned long long host = 0;
     FPX_CUDA(cudaMemcpyAsync(&host, status, sizeof host, cudaMemcpyDeviceToHost, s));
@@ -248,6 +318,31 @@ int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, 
     if (code == FPX_ERR_INVALID_VALUE) return fail(code, "row %llu contains NaN", row);
     return fail(code, "row %llu scale does not fit in fp16 (or its 2^%d-folded effective scale overflows)", row,
                 15 - bias_of(e));
+}
+
+// ---------------------------------------------------------------- codes -> W
+int fpx_dequantize_codes(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int e, int m,
+                         uint16_t* w_f16, uint64_t* status_dev, fpx_stream_t stream) {
+    if (fpx_format_check(e, m)) return FPX_ERR_INVALID_FORMAT;
+    if (rows_p == 0 || cols_p == 0 || rows_p % 64 || cols_p % 64)
+        return fail(FPX_ERR_SHAPE_MISMATCH, "quantized dims must be multiples of 64");
+    if (!codes || !scales || !w_f16) return fail(FPX_ERR_INVALID_VALUE, "null buffer");
+    if ((reinterpret_cast<uintptr_t>(codes) | reinterpret_cast<uintptr_t>(w_f16)) % 16u)
+        return fail(FPX_ERR_INVALID_VALUE, "codes and w_f16 must be 16-byte aligned");
+    if (int st = check_device(false)) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
+    const bool own = status == nullptr;
+    if (own) FPX_CUDA(cudaMallocAsync(&status, sizeof(unsigned long long), s));
+    FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
+    FPX_CUDA(launch_dequant_codes(codes, scales, rows_p, cols_p, e, m, status, w_f16, s));
+    if (!own) return FPX_OK;
+    unsigned long long host = 0;
+    FPX_CUDA(cudaMemcpyAsync(&host, status, sizeof host, cudaMemcpyDeviceToHost, s));
+    FPX_CUDA(cudaFreeAsync(status, s));
+    FPX_CUDA(cudaStreamSynchronize(s));
+    if (host == ~0ull) return FPX_OK;
+    return fail(FPX_ERR_INVALID_CODE, "row %llu holds a code out of range for e%dm%d", host >> 8, e, m);
 }
 
 // ---------------------------------------------------------------- K0+K1 fused
@@ -278,6 +373,7 @@ int fpx_quantize_pack(const void* w, int dtype, uint32_t rows, uint32_t cols, in
     uint8_t* sp[3] = {streams[0], ns > 1 ? streams[1] : nullptr, ns > 2 ? streams[2] : nullptr};
     FPX_CUDA(launch_quantize_pack(w, dtype, rows, cols, rows_p, cols_p, e, m, maxrep, scales, status,
                                   scratch + skip_off, ns, wv, sp, s));
+    mark_weights_written(s);
     if (!own) {
         FPX_CUDA(cudaFreeAsync(scratch, s));
         return FPX_OK;
@@ -318,6 +414,7 @@ int fpx_prepack(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, u
         if (hb) return fail(FPX_ERR_SCALE_OVERFLOW, "effective scale overflows fp16");
     }
     FPX_CUDA(launch_prepack(codes, rows_p, cols_p, 1 + e + m, ns, w, streams, s));
+    mark_weights_written(s);
     return FPX_OK;
 }
 
@@ -440,6 +537,7 @@ static int linear_impl(const uint8_t* const* streams, int nseg, const uint16_t* 
     float* part = reinterpret_cast<float*>(ws + lay.part_off);
     const char* g = std::getenv("FPX_LINEAR_GRID");
     const int grid = g ? std::atoi(g) : num_sms();
+    const uint32_t pdl_cap = take_weights_written(s) ? 1u : 2u;
     const uint32_t chunk = 256u;  // widest accumulator of the fused kernels
     for (uint32_t n0 = 0; n0 < n; n0 += chunk) {
         LinearLaunch L{};
@@ -468,10 +566,26 @@ static int linear_impl(const uint8_t* const* streams, int nseg, const uint16_t* 
         L.grid = grid;
         L.trace = debug_trace_buffer();
         L.prog = debug_progress_buffer();
+        L.pdl_cap = pdl_cap;
         const cudaError_t err = launch_linear(L, s);
-        if (err == cudaErrorNotSupported) return fail(FPX_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
-        if (err != cudaSuccess) return cuda_fail(err, "fpx_linear_kernel launch");
+        if (err != cudaSuccess) {
+            // A launch that did not run to completion may leave split-K
+            // arrival counters behind; clear them so the workspace stays
+            // valid for the next call (a sticky device fault makes every
+            // later call fail anyway).
+            (void)cudaGetLastError();
+            if (split_k > 1) (void)cudaMemsetAsync(counters, 0, kLinearCounterBytes, s);
+            if (err == cudaErrorNotSupported) return fail(FPX_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+            return cuda_fail(err, "fpx_linear_kernel launch");
+        }
     }
+    return FPX_OK;
+}
+
+int fpx_linear_workspace_reset(void* workspace, size_t workspace_bytes, fpx_stream_t stream) {
+    if (workspace == nullptr || workspace_bytes < kLinearCounterBytes)
+        return fail(FPX_ERR_INVALID_VALUE, "workspace of at least %zu bytes required", kLinearCounterBytes);
+    FPX_CUDA(cudaMemsetAsync(workspace, 0, kLinearCounterBytes, reinterpret_cast<cudaStream_t>(stream)));
     return FPX_OK;
 }
 

@@ -399,6 +399,57 @@ __global__ void __launch_bounds__(32 * kPackWarps) dequant_lut_kernel(SplitDescC
     }
 }
 
+// dequantize_reference straight from the code matrix (codec.cpp:179-193):
+// W[r][c] = half_mul(fp16(decode(code)), scale[r]) for every padded element.
+// HBM-bound (1 B in, 2 B out per element): each thread turns 16 codes (one
+// 16-byte load) into 16 fp16 (two 16-byte stores) through a shared LUT of
+// fp16(decode(code)); a code with bits above the format's width (the
+// reference's decode_scalar InvalidCode, codec.cpp:50-53) folds its row into
+// the atomicMin error key like quantize.
+__global__ void __launch_bounds__(256) dequant_codes_kernel(const uint8_t* __restrict__ codes,
+                                                            const uint16_t* __restrict__ scales, uint32_t cols_p,
+                                                            size_t nvec, int e, int m,
+                                                            unsigned long long* __restrict__ status,
+                                                            uint16_t* __restrict__ out) {
+    __shared__ uint16_t lut[256];
+    const int bits = 1 + e + m, bias = (1 << (e - 1)) - 1;
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+        const int sg = (c >> (e + m)) & 1, ef = (c >> m) & ((1 << e) - 1), mf = c & ((1 << m) - 1);
+        const float v = ef == 0 ? ldexpf(static_cast<float>(mf), 1 - bias - m)
+                                : ldexpf(static_cast<float>((1 << m) | mf), ef - bias - m);
+        lut[c] = __half_as_ushort(__float2half_rn(sg ? -v : v));
+    }
+    __syncthreads();
+    const uint32_t bad_mask = ~((1u << bits) - 1u) & 0xffu;
+    const uint32_t vec_per_row = cols_p / 16u;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nvec;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint4 cw = __ldcs(reinterpret_cast<const uint4*>(codes) + i);
+        const size_t row = i / vec_per_row;
+        const __half2 s2 = __half2half2(__ushort_as_half(__ldg(&scales[row])));
+        const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+        uint32_t o[8];
+        uint32_t any_bad = 0;
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+            const uint32_t w = words[wi];
+            any_bad |= w & (bad_mask * 0x01010101u);
+#pragma unroll
+            for (int hp = 0; hp < 2; ++hp) {
+                const uint32_t lo = lut[(w >> (16 * hp)) & 0xffu], hi = lut[(w >> (16 * hp + 8)) & 0xffu];
+                const __half2 d = __halves2half2(__ushort_as_half(static_cast<uint16_t>(lo)),
+                                                 __ushort_as_half(static_cast<uint16_t>(hi)));
+                const __half2 r = __hmul2_rn(d, s2);  // fp16 RNE product, subnormals kept (half.cpp:68-70)
+                o[2 * wi + hp] = *reinterpret_cast<const uint32_t*>(&r);
+            }
+        }
+        if (any_bad) atomicMin(status, (static_cast<unsigned long long>(row) << 8) | 2ull /* FPX_ERR_INVALID_CODE */);
+        uint4* dst = reinterpret_cast<uint4*>(out) + 2 * i;
+        __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        __stcs(dst + 1, make_uint4(o[4], o[5], o[6], o[7]));
+    }
+}
+
 // Scale-validity scan for pack (prepack.cpp:165-168): flags any row whose
 // effective scale is not finite.
 __global__ void check_scales_kernel(const uint16_t* __restrict__ scales, uint32_t n, int rebias,
@@ -452,6 +503,13 @@ __global__ void gather_shards_kernel(const float* __restrict__ g, uint32_t rows_
 }
 
 }  // namespace fpxk
+
+cudaError_t launch_dequant_codes(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int e,
+                                 int m, unsigned long long* status, uint16_t* out, cudaStream_t st) {
+    const size_t nvec = static_cast<size_t>(rows_p) * cols_p / 16u;
+    fpxk::dequant_codes_kernel<<<148 * 8, 256, 0, st>>>(codes, scales, cols_p, nvec, e, m, status, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gather_shards(const float* g, uint32_t rows_p, int world, uint32_t m_slot, uint32_t n, float* c,
                                  uint32_t ldc, cudaStream_t st) {

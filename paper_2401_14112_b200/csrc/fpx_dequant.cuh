@@ -107,7 +107,7 @@ FPX_DEV void cvt_pairs(uint32_t paired, uint32_t& lo, uint32_t& hi) {
 // Right shift on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF).  The
 // ALU pipe (LOP3/SHF/PRMT/F2FP, 16 lanes/clk/SMSP on B200) is what bounds
 // the de-quantiser; HMUL2/IMAD issue to the FMA pipe.  Measured by
-// tests/micro/pipe_bench.cu.
+// tools/micro/pipe_bench.cu.
 #ifndef FPX_SHR_ON_FMA
 #define FPX_SHR_ON_FMA 0
 #endif

@@ -5,6 +5,7 @@
 // gemm.cpp:20-30) so callers see the same fpx::Error codes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -68,7 +69,12 @@ struct DevBuf {
     }
 };
 
-uint16_t float_to_half_bits(float f) {
+}  // namespace
+
+// ------------------------------------------------------------------ half.hpp
+// half.cpp:7-70 semantics: exact widening, RNE narrowing with subnormals,
+// multiply = exact fp32 product narrowed once.
+uint16_t float_to_half(float f) {
     uint32_t x;
     std::memcpy(&x, &f, 4);
     const uint16_t s = static_cast<uint16_t>((x >> 16) & 0x8000u);
@@ -92,7 +98,7 @@ uint16_t float_to_half_bits(float f) {
     return static_cast<uint16_t>(s | base);
 }
 
-float half_bits_to_float(uint16_t h) {
+float half_to_float(uint16_t h) {
     const uint32_t s = uint32_t(h & 0x8000u) << 16, e = (h >> 10) & 31u, m = h & 1023u;
     float v;
     if (e == 0) v = std::ldexp(float(m), -24);
@@ -105,7 +111,7 @@ float half_bits_to_float(uint16_t h) {
     return v;
 }
 
-}  // namespace
+uint16_t half_mul(uint16_t a, uint16_t b) { return float_to_half(half_to_float(a) * half_to_float(b)); }
 
 // ------------------------------------------------------------------ errors
 const char* error_code_name(ErrorCode c) { return fpx_status_name(static_cast<int>(c) + 1); }
@@ -118,6 +124,14 @@ std::string Error::formatted() const {
 
 // ------------------------------------------------------------------ formats
 float FpxFormat::max_representable() const { return fpx_max_representable(exp_bits, man_bits); }
+
+float FpxFormat::ulp_at(double magnitude) const {
+    magnitude = std::fabs(magnitude);
+    const int e_min = 1 - bias(), e_max = (1 << exp_bits) - 1 - bias();
+    int e = e_min;
+    if (magnitude >= std::ldexp(1.0, e_min)) e = std::min(static_cast<int>(std::floor(std::log2(magnitude))), e_max);
+    return static_cast<float>(std::ldexp(1.0, e - man_bits));
+}
 
 std::string FpxFormat::name() const { return "e" + std::to_string(exp_bits) + "m" + std::to_string(man_bits); }
 
@@ -173,15 +187,27 @@ ScalarMatrix ScalarMatrix::zeros(Dtype dt, Layout lo, uint32_t rows, uint32_t co
 ScalarMatrix to_fp32(const ScalarMatrix& m) {
     if (m.dtype == Dtype::Fp32) return m;
     ScalarMatrix out = ScalarMatrix::zeros(Dtype::Fp32, m.layout, m.rows, m.cols);
-    for (size_t i = 0; i < m.f16.size(); ++i) out.f32[i] = half_bits_to_float(m.f16[i]);
+    for (size_t i = 0; i < m.f16.size(); ++i) out.f32[i] = half_to_float(m.f16[i]);
     return out;
 }
 
 ScalarMatrix to_fp16(const ScalarMatrix& m) {
     if (m.dtype == Dtype::Fp16) return m;
     ScalarMatrix out = ScalarMatrix::zeros(Dtype::Fp16, m.layout, m.rows, m.cols);
-    for (size_t i = 0; i < m.f32.size(); ++i) out.f16[i] = float_to_half_bits(m.f32[i]);
+    for (size_t i = 0; i < m.f32.size(); ++i) out.f16[i] = float_to_half(m.f32[i]);
     return out;
+}
+
+float decode_scalar(uint32_t code, const FpxFormat& fmt) {
+    float v = 0.0f;
+    check(fpx_decode_scalar(code, fmt.exp_bits, fmt.man_bits, &v));
+    return v;
+}
+
+uint32_t encode_scalar(double value, const FpxFormat& fmt) {
+    uint32_t code = 0;
+    check(fpx_encode_scalar(value, fmt.exp_bits, fmt.man_bits, &code));
+    return code;
 }
 
 uint16_t effective_scale(uint16_t row_scale, const FpxFormat& fmt) {
@@ -294,6 +320,20 @@ ScalarMatrix dequantize(const PackedWeights& p) {
     return w;
 }
 
+ScalarMatrix dequantize_reference(const QuantizedMatrix& q) {
+    if (q.rows == 0 || q.cols == 0 || q.rows % 64 || q.cols % 64 || q.codes.size() != size_t(q.rows) * q.cols ||
+        q.scales.size() != q.rows)
+        throw Error(ErrorCode::ShapeMismatch, "quantized matrix must be padded to multiples of 64 with one scale per row");
+    DevBuf codes(q.codes.size()), scales(q.scales.size() * 2), out(q.codes.size() * 2);
+    codes.upload(q.codes.data(), q.codes.size());
+    scales.upload(q.scales.data(), q.scales.size() * 2);
+    check(fpx_dequantize_codes(codes.as<uint8_t>(), scales.as<uint16_t>(), q.rows, q.cols, q.format.exp_bits,
+                               q.format.man_bits, out.as<uint16_t>(), nullptr, nullptr));
+    ScalarMatrix w = ScalarMatrix::zeros(Dtype::Fp16, Layout::RowMajor, q.rows, q.cols);
+    out.download(w.f16.data(), w.f16.size() * 2);
+    return w;
+}
+
 // ------------------------------------------------------------------ K2
 static void check_problem(uint32_t a_cols, uint32_t a_orig_cols, const ScalarMatrix& b) {
     if (b.dtype != Dtype::Fp16 || b.layout != Layout::ColMajor)
@@ -353,11 +393,16 @@ ScalarMatrix gemm_packed(const PackedWeights& a, const ScalarMatrix& b, BankAcce
     return lin.forward(b);
 }
 
+ScalarMatrix gemm_reference(const QuantizedMatrix& q, const ScalarMatrix& b) {
+    check_problem(q.cols, q.orig_cols ? q.orig_cols : q.cols, b);
+    return gemm_packed(pack(q), b);
+}
+
 // ------------------------------------------------------------------ io.hpp
 // PackFile over the C-ABI container code (fpx_io.cpp); MatrixFile here.
 // Both little-endian with strict validation (SPEC.md model-io).
 namespace {
-constexpr char kMatMagic[8] = {'F', 'P', 'X', 'M', 'A', 'T', '1', 0};
+constexpr const char* kMatMagic = kMatrixMagic;
 
 template <typename T>
 void put(std::vector<uint8_t>& o, T v) {

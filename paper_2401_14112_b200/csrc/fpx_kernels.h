@@ -21,6 +21,8 @@ cudaError_t launch_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32
 cudaError_t launch_dequant(const uint8_t* const* streams, int nseg, const int* widths, const uint16_t* scales,
                            uint32_t rows_p, uint32_t cols_p, int e, int m, uint16_t* out, int path,
                            cudaStream_t st);
+cudaError_t launch_dequant_codes(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, uint32_t cols_p, int e,
+                                 int m, unsigned long long* status, uint16_t* out, cudaStream_t st);
 cudaError_t launch_check_scales(const uint16_t* scales, uint32_t n, int rebias, unsigned int* bad,
                                 cudaStream_t st);
 cudaError_t launch_stage_act(const uint16_t* src, uint32_t k_act, uint32_t n, uint32_t k_pad, uint16_t* dst,
@@ -53,6 +55,11 @@ struct LinearLaunch {
     const float* bias;         // rows_p, or null
     uint32_t act_fn;           // 0 none, 1 relu, 2 silu, 3 gelu (tanh)
     const void* resid;         // same dtype / layout / ldc as C, or null
+    // Upper bound on the programmatic-dependent-launch mode of this launch
+    // (see pdl_mode in fpx_linear.cu): 1 after a library kernel wrote packed
+    // weights / scales on the same stream, so nothing is read before
+    // griddepcontrol.wait; 2 = no cap.
+    uint32_t pdl_cap = 2;
 };
 
 cudaError_t launch_linear(const LinearLaunch& p, cudaStream_t st);

@@ -42,6 +42,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "fpx_dequant.cuh"
 #include "fpx_kernels.h"
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
 // ===========================================================================
 // Decode kernel (batch <= 32, the memory-bound regime).
 //
-// Measured constraints that shape it (tests/micro/, B200):
+// Measured constraints that shape it (tools/micro/, B200):
 //  * a kind::f16 tcgen05.mma with M=128, K=16 occupies the tensor pipe for
 //    ~44 cycles for ANY N <= 128 (operand fetch, not math, bounds it), i.e.
 //    at most ~46 fp16 weights/clk/SM -- only ~1.5x the ~31 weights/clk/SM
@@ -1159,9 +1161,6 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     if (p.split > 1) final_split_reduce<NPAD>(p, final_red, C::kThreads);
 }
 
-#ifndef FPX_CLASSIC_CAP
-#define FPX_CLASSIC_CAP 0
-#endif
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1173,6 +1172,22 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     });
     return fn;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-(function, device)
+// setting: a process driving several GPUs sets it once on each device it
+// launches on, and a failed attempt is retried on the next call.
+static cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;  // (kernel, device) pairs already configured
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& d : done)
+        if (d.first == kern && d.second == dev) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.emplace_back(kern, dev);
+    return e;
 }
 
 // Programmatic dependent launch (FPX_LINEAR_PDL, read once):
@@ -1196,7 +1211,7 @@ static uint32_t pdl_mode() {
 }
 
 template <typename Kern, typename... Args>
-cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t st, Args... args) {
+cudaError_t launch_pdl(bool pdl, Kern kern, int grid, int threads, int smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
@@ -1206,7 +1221,7 @@ cudaError_t launch_pdl(Kern kern, int grid, int threads, int smem, cudaStream_t 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_mode() != 0 ? 1 : 0;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -1254,20 +1269,10 @@ cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
     if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
     // NPAD = 256 (single accumulator buffer): the intermittent wrong results
     // once measured at split 9 were the stage-ring parity aliasing now ruled
-    // out by Cfg (kStages >= NG + kAStages); FPX_CLASSIC_CAP=1 restores the
-    // old cap at split 2 (the default split for this width anyway).
+    // out by Cfg (kStages >= NG + kAStages).
     KParams kq = kp;
-    if (FPX_CLASSIC_CAP && C::kAccBufs == 1 && kq.split > 2) {
-        kq.split = 2;
-        kq.units = (kp.rows_p + kTileM - 1) / kTileM * 2;
-    }
     if (C::kAccBufs == 1) grid = static_cast<int>(kq.units);
-    static std::once_flag attr_once;  // per instantiation (the attribute is per function)
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::kSmemBytes)) return e;
     kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(map, kq);
     return cudaGetLastError();
 }
@@ -1290,47 +1295,33 @@ cudaError_t launch_g(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
         return e;
     if (cudaError_t e = make_stream_map(L.s_lo, FmtTraits<F>::kBitsLo, L.rows_p / 64, L.cols_p / 64, C::kKS, &lo_map))
         return e;
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
-    kq.pdl = pdl_mode();
-    return launch_pdl(kern, grid, C::kThreads, C::kSmemBytes, st, map, hi_map, lo_map, kq);
+    if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::kSmemBytes)) return e;
+    kq.pdl = std::min(pdl_mode(), L.pdl_cap);
+    return launch_pdl(kq.pdl != 0, kern, grid, C::kThreads, C::kSmemBytes, st, map, hi_map, lo_map, kq);
 }
 
-// Pipeline shape per batch width.  N <= 32 (decode): the grouped kernel,
-// KS k-tiles per stage, G self-issuing de-quantiser groups.  N > 32: the
-// single-issuer kernel, KS k-tiles per stage, NG de-quantiser groups.
-// Tuning overrides (instantiated subset only): FPX_LINEAR_KERNEL=classic
-// forces the single-issuer kernel for N <= 32; FPX_LINEAR_CFG="KS,G".
+// Pipeline shape per batch width.  N <= 128: the decode kernel, KS k-tiles
+// per stage, G de-quantiser groups (8192x22016: N=64 35.0 us vs 37.8 us,
+// N=128 53.0 us vs 56.7 us for the single-issuer kernel at its best split;
+// NPAD=128 runs 3 groups, 4 measured equal).  N > 128: the single-issuer
+// kernel in 256-column chunks.  Tuning override (instantiated subset only):
+// FPX_LINEAR_CFG="KS,G" at NPAD 16 / 32.
 template <int F>
 cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, int grid, cudaStream_t st) {
     int ks = 0, ng = 0;
     if (const char* c = std::getenv("FPX_LINEAR_CFG")) std::sscanf(c, "%d,%d", &ks, &ng);
-    const char* kname = std::getenv("FPX_LINEAR_KERNEL");
-    const bool classic = kname != nullptr && std::strcmp(kname, "classic") == 0;
-    if (!classic && npad <= 32) {
-        if (npad <= 16) {
-            if (ks == 1 && ng == 4) return launch_g<F, 16, 1, 4>(L, kp, grid, st);
-            if (ks == 2 && ng == 3) return launch_g<F, 16, 2, 3>(L, kp, grid, st);
-            if (ks == 2 && ng == 5) return launch_g<F, 16, 2, 5>(L, kp, grid, st);
-            return launch_g<F, 16, 2, 4>(L, kp, grid, st);
-        }
-        if (npad == 32) {
-            if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
-            return launch_g<F, 32, 2, 4>(L, kp, grid, st);
-        }
+    if (npad <= 16) {
+        if (ks == 1 && ng == 4) return launch_g<F, 16, 1, 4>(L, kp, grid, st);
+        if (ks == 2 && ng == 3) return launch_g<F, 16, 2, 3>(L, kp, grid, st);
+        if (ks == 2 && ng == 5) return launch_g<F, 16, 2, 5>(L, kp, grid, st);
+        return launch_g<F, 16, 2, 4>(L, kp, grid, st);
     }
-    // 32 < N <= 128: the decode kernel as well (8192x22016: N=64 35.0 us vs
-    // 37.8 us, N=128 53.0 us vs 56.7 us for the single-issuer kernel at its
-    // best split).  NPAD=128 runs 3 de-quantiser groups (4 measured equal).
+    if (npad == 32) {
+        if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
+        return launch_g<F, 32, 2, 4>(L, kp, grid, st);
+    }
     if (npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
     if (npad == 128) return launch_g<F, 128, 2, 3>(L, kp, grid, st);
-    (void)classic;  // N <= 128 always runs the decode kernel
-    if (npad <= 16) return launch_g<F, 16, 2, 4>(L, kp, grid, st);
-    if (npad == 32) return launch_g<F, 32, 2, 4>(L, kp, grid, st);
     if (npad == 256) return launch_t<F, 256, 1, 2>(L, kp, grid, st);
     return cudaErrorInvalidValue;
 }

@@ -199,6 +199,12 @@ def _stream(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _on(device: torch.device):
+    """Make `device` current around a C-ABI call: the library queries the
+    current device (sm_100 gate, SM count, per-device kernel attributes)."""
+    return torch.cuda.device(device)
+
+
 def pad64(n: int) -> int:
     return (n + 63) // 64 * 64
 
@@ -229,8 +235,9 @@ def quantize_matrix(m: torch.Tensor, fmt: FpxFormat) -> QuantizedMatrix:
     rp, cp = pad64(rows), pad64(cols)
     codes = torch.empty((rp, cp), dtype=torch.uint8, device=m.device)
     scales = torch.empty((rp,), dtype=torch.int16, device=m.device)
-    _check(L.fpx_quantize(m.data_ptr(), dt, rows, cols, fmt.exp_bits, fmt.man_bits, codes.data_ptr(),
-                          scales.data_ptr(), None, _stream(m.device)))
+    with _on(m.device):
+        _check(L.fpx_quantize(m.data_ptr(), dt, rows, cols, fmt.exp_bits, fmt.man_bits, codes.data_ptr(),
+                              scales.data_ptr(), None, _stream(m.device)))
     return QuantizedMatrix(fmt, rp, cp, rows, cols, codes, scales)
 
 
@@ -243,8 +250,9 @@ def pack(q: QuantizedMatrix, split: SplitScheme | None = None) -> PackedWeights:
                for w in split.widths]
     wid = (C.c_int * len(split.widths))(*split.widths)
     ptrs = (C.c_void_p * len(streams))(*[s.data_ptr() for s in streams])
-    _check(L.fpx_prepack(q.codes.data_ptr(), q.scales.data_ptr(), q.rows, q.cols, q.format.exp_bits,
-                         q.format.man_bits, wid, len(split.widths), ptrs, _stream(dev)))
+    with _on(dev):
+        _check(L.fpx_prepack(q.codes.data_ptr(), q.scales.data_ptr(), q.rows, q.cols, q.format.exp_bits,
+                             q.format.man_bits, wid, len(split.widths), ptrs, _stream(dev)))
     return PackedWeights(q.format, split, q.rows, q.cols, q.orig_rows or q.rows, q.orig_cols or q.cols, streams,
                          q.scales.clone())
 
@@ -265,9 +273,10 @@ def quantize_pack(m: torch.Tensor, fmt: FpxFormat, split: SplitScheme | None = N
     scales = torch.empty((rp,), dtype=torch.int16, device=m.device)
     wid = (C.c_int * len(split.widths))(*split.widths)
     ptrs = (C.c_void_p * len(streams))(*[s.data_ptr() for s in streams])
-    _check(L.fpx_quantize_pack(m.data_ptr(), 0 if m.dtype == torch.float32 else 1, rows, cols, fmt.exp_bits,
-                               fmt.man_bits, wid, len(split.widths), ptrs, scales.data_ptr(), None,
-                               _stream(m.device)))
+    with _on(m.device):
+        _check(L.fpx_quantize_pack(m.data_ptr(), 0 if m.dtype == torch.float32 else 1, rows, cols, fmt.exp_bits,
+                                   fmt.man_bits, wid, len(split.widths), ptrs, scales.data_ptr(), None,
+                                   _stream(m.device)))
     return PackedWeights(fmt, split, rp, cp, rows, cols, streams, scales)
 
 
@@ -278,8 +287,9 @@ def unpack(p: PackedWeights) -> QuantizedMatrix:
     codes = torch.empty((p.rows, p.cols), dtype=torch.uint8, device=dev)
     wid = (C.c_int * len(p.split.widths))(*p.split.widths)
     ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
-    _check(L.fpx_unpack(ptrs, p.rows, p.cols, p.format.exp_bits, p.format.man_bits, wid, len(p.split.widths),
-                        codes.data_ptr(), _stream(dev)))
+    with _on(dev):
+        _check(L.fpx_unpack(ptrs, p.rows, p.cols, p.format.exp_bits, p.format.man_bits, wid, len(p.split.widths),
+                            codes.data_ptr(), _stream(dev)))
     return QuantizedMatrix(p.format, p.rows, p.cols, p.orig_rows, p.orig_cols, codes, p.scales.clone())
 
 
@@ -291,8 +301,9 @@ def dequantize(p: PackedWeights) -> torch.Tensor:
     out = torch.empty((p.rows, p.cols), dtype=torch.float16, device=dev)
     wid = (C.c_int * len(p.split.widths))(*p.split.widths)
     ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
-    _check(L.fpx_dequantize(ptrs, len(p.streams), wid, p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
-                            p.format.man_bits, out.data_ptr(), _stream(dev)))
+    with _on(dev):
+        _check(L.fpx_dequantize(ptrs, len(p.streams), wid, p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                                p.format.man_bits, out.data_ptr(), _stream(dev)))
     return out
 
 
@@ -331,25 +342,37 @@ def gemm_packed(p: PackedWeights, b: torch.Tensor, *, out: torch.Tensor | None =
     L = _lib.load()
     if b.dtype != torch.float16 or b.dim() != 2:
         raise FpxError(5, "error[shape-mismatch] activations must be fp16 col-major")
+    dev = p.streams[0].device
+    if not b.is_cuda or b.device != dev:
+        raise FpxError(3, f"error[invalid-value] activations must live on the weights' device {dev}")
     n, k_act = b.shape
     if k_act != p.cols and k_act != p.orig_cols:
         raise FpxError(5, f"error[shape-mismatch] weight cols {p.cols} (orig {p.orig_cols}) do not match "
                           f"activation rows {k_act}")
     b = b.contiguous()
-    dev = b.device
-    ldc = ldc or p.rows
     if out is None:
+        ldc = ldc or p.rows
         out = torch.empty((n, ldc), dtype=torch.float32, device=dev)
+    else:
+        if out.dtype != torch.float32 or out.dim() != 2 or not out.is_contiguous() or out.device != dev:
+            raise FpxError(5, "error[shape-mismatch] out must be a contiguous fp32 [N, ldc] tensor on the weights' "
+                              "device")
+        if ldc is not None and ldc != out.shape[1]:
+            raise FpxError(5, f"error[shape-mismatch] ldc {ldc} != out.shape[1] {out.shape[1]}")
+        ldc = out.shape[1]
+        if out.shape[0] != n or ldc < p.rows:
+            raise FpxError(5, f"error[shape-mismatch] out must be [{n}, >= {p.rows}], got {list(out.shape)}")
     if n == 0:
         return out
     sk = split_k if split_k > 0 else default_split(p.rows, p.cols, n)
     misaligned = b.data_ptr() % 16 != 0
-    need = int(L.fpx_linear_workspace_size(p.rows, p.cols, k_act + (1 if misaligned else 0), n, sk))
-    ws = linear_workspace(dev, need)
-    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
-    _check(L.fpx_linear(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
-                        p.format.man_bits, b.data_ptr(), k_act, n, out.data_ptr(), ldc, sk,
-                        _ptr(ws), 0 if ws is None else ws.numel(), _stream(dev)))
+    with _on(dev):
+        need = int(L.fpx_linear_workspace_size(p.rows, p.cols, k_act + (1 if misaligned else 0), n, sk))
+        ws = linear_workspace(dev, need)
+        ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+        _check(L.fpx_linear(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                            p.format.man_bits, b.data_ptr(), k_act, n, out.data_ptr(), ldc, sk,
+                            _ptr(ws), 0 if ws is None else ws.numel(), _stream(dev)))
     return out
 
 
@@ -419,7 +442,8 @@ def read_pack_file(path: str, device: str | torch.device = "cuda") -> PackedWeig
     scales = torch.empty(h.rows_p, dtype=torch.int16, device=dev)
     streams = [torch.empty(h.stream_bytes[i], dtype=torch.uint8, device=dev) for i in range(h.nseg)]
     ptrs = (C.c_void_p * h.nseg)(*[t.data_ptr() for t in streams])
-    _check(L.fpx_packfile_load(path.encode(), C.byref(h), scales.data_ptr(), ptrs, _stream(dev)))
+    with _on(dev):
+        _check(L.fpx_packfile_load(path.encode(), C.byref(h), scales.data_ptr(), ptrs, _stream(dev)))
     return _from_header(h, scales, streams)
 
 
@@ -437,6 +461,8 @@ def linear(act: torch.Tensor, p: PackedWeights, *, bias: torch.Tensor | None = N
     L = _lib.load()
     if act.dtype != torch.float16 or act.dim() != 2 or not act.is_cuda:
         raise FpxError(3, "error[invalid-value] activations must be a CUDA fp16 [N, K] tensor")
+    if act.device != p.streams[0].device:
+        raise FpxError(3, f"error[invalid-value] activations must live on the weights' device {p.streams[0].device}")
     if out_dtype not in (torch.float16, torch.float32):
         raise FpxError(3, "error[invalid-value] out_dtype must be float16 or float32")
     act = act.contiguous()
@@ -457,12 +483,14 @@ def linear(act: torch.Tensor, p: PackedWeights, *, bias: torch.Tensor | None = N
     if activation not in ACTIVATIONS:
         raise FpxError(3, f"error[invalid-value] activation must be one of {sorted(k for k in ACTIVATIONS if k)}")
     epi = _lib.Epilogue(1 if out_dtype == torch.float16 else 0, _ptr(bias), ACTIVATIONS[activation], _ptr(residual))
-    ws_bytes = int(L.fpx_linear_workspace_size(p.rows, p.cols, k, n, split_k))
-    ws = linear_workspace(dev, ws_bytes)
-    ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
-    _check(L.fpx_linear_ex(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
-                           p.format.man_bits, act.data_ptr(), k, n, out.data_ptr(), p.rows, split_k, C.byref(epi),
-                           _ptr(ws), ws_bytes, _stream(dev)))
+    with _on(dev):
+        misaligned = act.data_ptr() % 16 != 0
+        ws_bytes = int(L.fpx_linear_workspace_size(p.rows, p.cols, k + (1 if misaligned else 0), n, split_k))
+        ws = linear_workspace(dev, ws_bytes)
+        ptrs = (C.c_void_p * len(p.streams))(*[s.data_ptr() for s in p.streams])
+        _check(L.fpx_linear_ex(ptrs, len(p.streams), p.scales.data_ptr(), p.rows, p.cols, p.format.exp_bits,
+                               p.format.man_bits, act.data_ptr(), k, n, out.data_ptr(), p.rows, split_k, C.byref(epi),
+                               _ptr(ws), ws_bytes, _stream(dev)))
     return out
 
 

@@ -58,8 +58,9 @@ def cuda_permute(gathered: torch.Tensor, row0, nrows, m_slot: int, n: int, out: 
     dev = gathered.device
     r0 = torch.tensor(row0, dtype=torch.int32, device=dev)
     nr = torch.tensor(nrows, dtype=torch.int32, device=dev)
-    _check(L.fpx_gather_permute(gathered.data_ptr(), r0.data_ptr(), nr.data_ptr(), len(row0), m_slot, n,
-                                out.data_ptr(), out.shape[1], torch.cuda.current_stream(dev).cuda_stream))
+    with torch.cuda.device(dev):
+        _check(L.fpx_gather_permute(gathered.data_ptr(), r0.data_ptr(), nr.data_ptr(), len(row0), m_slot, n,
+                                    out.data_ptr(), out.shape[1], torch.cuda.current_stream(dev).cuda_stream))
     return out
 
 
@@ -89,8 +90,13 @@ def sharded_linear(p: PackedWeights, b: torch.Tensor, rank: int, world: int, gro
     [n, m_local] slice."""
     n = b.shape[0]
     sk = split_k or default_split(p.rows, p.cols, n)
-    local = local_shard(p, rank, world)
-    c_local = compute(local, b, split_k=sk)
+    tr0, tr1 = shard_tile_rows(p.rows, rank, world)
+    if tr1 > tr0:
+        c_local = compute(p.shard(tr0, tr1), b, split_k=sk)
+    else:
+        # more ranks than tile-rows: this rank owns nothing but must still
+        # join the collective, or the other ranks block in all_gather forever
+        c_local = torch.empty((n, 0), dtype=torch.float32, device=b.device)
     if not gather or world == 1:
         return c_local
     return gather_output(c_local, p.rows, rank, world, group, permute=permute)

@@ -75,6 +75,57 @@ def test_effective_scale_exhaustive(oracle, e, m):
             assert a == b, (e, m, hex(s))
 
 
+ALL_FORMATS = [(e, m) for e in range(1, 6) for m in range(0, 7) if 3 <= 1 + e + m <= 8]
+
+
+def test_scalar_codec_matches_reference_exhaustively(oracle):
+    """fpx_decode_scalar / fpx_encode_scalar (codec.hpp:56,60) against the
+    reference itself (oracle/_ref) when built, else the pinned C oracle: every
+    code of every format, and 20k random doubles per format spanning
+    subnormals, ties, saturation and signed zeros."""
+    from oracle.oracle import REF_SO, Reference
+    ref = Reference() if os.path.exists(REF_SO) else None
+    dec = (lambda c, e, m: ref.lib.ref_decode(c, e, m)) if ref else oracle.decode
+    enc = (lambda v, e, m: ref.lib.ref_encode(v, e, m)) if ref else oracle.encode
+    L = _lib.load()
+    f = C.c_float()
+    u = C.c_uint32()
+    rng = np.random.default_rng(56)
+    for e, m in ALL_FORMATS:
+        for code in range(1 << (1 + e + m)):
+            assert L.fpx_decode_scalar(code, e, m, C.byref(f)) == 0
+            assert f.value == dec(code, e, m) or (np.isnan(f.value) and np.isnan(dec(code, e, m))), (e, m, code)
+            assert L.fpx_encode_scalar(f.value, e, m, C.byref(u)) == 0 and u.value == code, (e, m, code)
+        assert L.fpx_decode_scalar(1 << (1 + e + m), e, m, C.byref(f)) == 1 + fpx.ErrorCode.InvalidCode
+        maxrep = L.fpx_max_representable(e, m)
+        vals = np.concatenate([rng.standard_normal(8000) * maxrep / 4, rng.uniform(-2 * maxrep, 2 * maxrep, 8000),
+                               rng.standard_normal(4000) * 2.0 ** (2 - (1 << (e - 1)) - m), [0.0, -0.0, np.inf, -np.inf]])
+        # exact ties: midpoints between neighbouring codes
+        grid = np.array([dec(c, e, m) for c in range(1 << (e + m))], dtype=np.float64)
+        vals = np.concatenate([vals, (grid[:-1] + grid[1:]) / 2, -(grid[:-1] + grid[1:]) / 2])
+        for v in vals:
+            assert L.fpx_encode_scalar(float(v), e, m, C.byref(u)) == 0
+            assert u.value == enc(float(v), e, m), (e, m, float(v))
+    assert L.fpx_encode_scalar(float("nan"), 3, 2, C.byref(u)) == 1 + fpx.ErrorCode.InvalidValue
+    assert b"invalid-value" in L.fpx_last_error()
+
+
+def test_ref_api_caller_compiles_and_runs_host_checks():
+    """A caller written only against the reference's headers (fpx/codec.hpp,
+    fpx/gemm.hpp, ... -> include/fpx/*.hpp) builds and links; without a GPU
+    its host-side checks (scalar KATs, formats, half helpers) all pass before
+    the first device call reports the device error."""
+    exe = os.path.join(ROOT, "paper_2401_14112_b200", "build", "fpx_ref_api_caller")
+    assert os.path.exists(exe), "built by `make -C paper_2401_14112_b200`"
+    src = open(os.path.join(ROOT, "paper_2401_14112_b200", "csrc", "tools", "fpx_ref_api_caller.cpp")).read()
+    assert '#include "fpx/codec.hpp"' in src and "fpx_c.h" not in src and "fpx_b200.hpp" not in src
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("exercised by the gpu tests")
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 3 and "FAIL" not in r.stdout, r.stdout + r.stderr
+
+
 def test_default_split_matches_measured_best():
     """fpx_linear_default_split (waves x (k-tiles per unit + ~10 k-tile
     per-unit overhead)) picks the split measured fastest on B200 for SURVEY
@@ -196,4 +247,3 @@ def test_cpp_dropin_wrapper_compiles_and_links():
         pytest.skip("exercised by the gpu tests")
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 3 and ("error[device]" in r.stdout or "error[cuda]" in r.stdout), r.stdout + r.stderr
-    np.testing.assert_equal(1, 1)

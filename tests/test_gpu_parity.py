@@ -585,3 +585,164 @@ def test_pdl_back_to_back_stress(cuda, n):
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+# ------------------------------------------------------------ drop-in boundary (round 2)
+@pytest.mark.parametrize("e,m", [(3, 2), (2, 3), (2, 2), (4, 3), (2, 1)])
+def test_dequantize_codes_exhaustive(cuda, oracle, e, m):
+    """fpx_dequantize_codes == dequantize_reference (codec.cpp:179-193) for
+    every code x 1024 fp16 scale patterns (incl. zero, negative, subnormal,
+    inf/NaN payload scales), bit for bit; an out-of-range code is
+    InvalidCode naming the first failing row."""
+    import ctypes as C
+    fpx = _fpx()
+    L = fpx._lib.load()
+    ncode = 1 << (1 + e + m)
+    rows, cols = 1024, 256
+    rng = np.random.default_rng(e * 7 + m)
+    codes = np.tile(np.arange(cols, dtype=np.uint32) % ncode, (rows, 1)).astype(np.uint8)
+    scales = np.concatenate([np.arange(0, 1 << 16, 64, dtype=np.uint32)[:rows - 8],
+                             [0x0001, 0x8001, 0x03FF, 0x7BFF, 0xFBFF, 0x7C00, 0x7E00, 0x0000]]).astype(np.uint16)
+    rng.shuffle(scales)
+    d_codes = torch.from_numpy(codes).to(cuda)
+    d_scales = torch.from_numpy(scales.view(np.int16)).to(cuda)
+    out = torch.empty((rows, cols), dtype=torch.int16, device=cuda)
+    st = L.fpx_dequantize_codes(d_codes.data_ptr(), d_scales.data_ptr(), rows, cols, e, m, out.data_ptr(), None,
+                                torch.cuda.current_stream().cuda_stream)
+    assert st == 0, L.fpx_last_error()
+    assert (out.cpu().numpy().view(np.uint16) == oracle.dequantize(codes, scales, e, m)).all()
+    if ncode < 256:
+        bad = codes.copy()
+        bad[300, 17] = ncode
+        bad[700, 3] = 0xFF
+        d_bad = torch.from_numpy(bad).to(cuda)
+        st = L.fpx_dequantize_codes(d_bad.data_ptr(), d_scales.data_ptr(), rows, cols, e, m, out.data_ptr(), None,
+                                    torch.cuda.current_stream().cuda_stream)
+        assert st == 1 + fpx.ErrorCode.InvalidCode and b"row 300" in L.fpx_last_error()
+
+
+def test_ref_api_caller_against_reference(cuda, tmp_path, oracle):
+    """The reference-API caller (reference headers only, linked to
+    libfpx_b200.so) passes its own checks on the GPU, and its outputs match
+    the reference itself on the same inputs: quantize codes/scales and pack
+    bytes bit-exact, dequantize_reference bit-exact, C within the bar."""
+    exe = os.path.join(ROOT, "paper_2401_14112_b200", "build", "fpx_ref_api_caller")
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows, cols, n, rp, cp = 200, 330, 24, 256, 384
+    rd = lambda name, dt: np.fromfile(tmp_path / name, dtype=dt)  # noqa: E731
+    w = rd("w_f32.bin", np.float32).reshape(rows, cols)
+    b = rd("b_f16.bin", np.uint16).reshape(n, cols)
+    from oracle.oracle import REF_SO, Reference
+    if os.path.exists(REF_SO):
+        R = Reference()
+        st, codes, scales = R.quantize(w, 3, 2)
+        assert st == 0
+        st, streams = R.pack(codes, scales, 3, 2, rows, cols)
+        st2, wq = R.dequantize(codes, scales, 3, 2)
+        c_ref = R.gemm_reference(codes, scales, 3, 2, b, orig_cols=cols, orig_rows=rows)
+    else:
+        st, codes, scales, _ = oracle.quantize(w, 3, 2)
+        st, streams = oracle.pack(codes, scales, 3, 2)
+        wq = oracle.dequantize(codes, scales, 3, 2)
+        st, c_ref = oracle.gemm_reference(codes, scales, 3, 2, b, orig_cols=cols)
+    assert (rd("codes.bin", np.uint8).reshape(rp, cp) == codes).all()
+    assert (rd("scales.bin", np.uint16) == scales).all()
+    assert (rd("stream0.bin", np.uint8) == streams[0]).all() and (rd("stream1.bin", np.uint8) == streams[1]).all()
+    assert (rd("wq_f16.bin", np.uint16).reshape(rp, cp) == wq).all()
+    assert rel_err(rd("c_f32.bin", np.float32).reshape(n, rp), c_ref) <= TOL
+
+
+def test_pdl_guard_after_async_weight_writers(cuda):
+    """PDL mode 2 streams weights before griddepcontrol.wait.  A linear that
+    directly follows an ASYNC fpx_quantize_pack (status_dev given) on the
+    same stream must still see the freshly written weights: the library caps
+    that launch at mode 1.  Weights alternate between two sources every
+    iteration, eagerly and inside a replayed CUDA graph."""
+    import ctypes as C
+    fpx = _fpx()
+    L = fpx._lib.load()
+    torch.manual_seed(21)
+    rows, cols, n = 4096, 8192, 16
+    srcs = [torch.randn(rows, cols, device=cuda) * 0.02 for _ in range(2)]
+    x = torch.randn(n, cols, device=cuda).half()
+    refs = [fpx.gemm_packed(fpx.quantize_pack(s, fpx.FpxFormat.e3m2()), x) for s in srcs]
+    assert not torch.equal(refs[0], refs[1])
+    streams = [torch.empty(L.fpx_stream_bytes(rows, cols, w), dtype=torch.uint8, device=cuda) for w in (2, 4)]
+    scales = torch.empty(rows, dtype=torch.int16, device=cuda)
+    status = torch.empty(1, dtype=torch.int64, device=cuda)
+    ptrs = (C.c_void_p * 2)(*[s.data_ptr() for s in streams])
+    split = fpx.default_split(rows, cols, n)
+    ws_n = int(L.fpx_linear_workspace_size(rows, cols, cols, n, split))
+    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
+    outs = [torch.empty(n, rows, device=cuda) for _ in range(2)]
+
+    def step(i):
+        s = torch.cuda.current_stream().cuda_stream
+        assert L.fpx_quantize_pack(srcs[i % 2].data_ptr(), 0, rows, cols, 3, 2, None, 0, ptrs, scales.data_ptr(),
+                                   status.data_ptr(), s) == 0
+        assert L.fpx_linear(ptrs, 2, scales.data_ptr(), rows, cols, 3, 2, x.data_ptr(), cols, n,
+                            outs[i % 2].data_ptr(), rows, split, ws.data_ptr(), ws_n, s) == 0, L.fpx_last_error()
+
+    for i in range(12):
+        step(i)
+        if i % 2 == 1:
+            torch.cuda.synchronize()
+            assert torch.equal(outs[0], refs[0]) and torch.equal(outs[1], refs[1]), i
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(6):
+            step(i)
+    for _ in range(3):
+        outs[0].zero_()
+        outs[1].zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], refs[0]) and torch.equal(outs[1], refs[1])
+    assert int(status.item()) == -1  # no failing row
+
+
+def test_workspace_reset_recovers_stale_counters(cuda):
+    """A workspace whose split-K arrival counters hold garbage (e.g. reused
+    for other data) gives wrong results until fpx_linear_workspace_reset."""
+    fpx = _fpx()
+    L = fpx._lib.load()
+    torch.manual_seed(8)
+    p = fpx.pack(fpx.quantize_matrix(torch.randn(2048, 4096, device=cuda) * 0.02, fpx.FpxFormat.e3m2()))
+    x = torch.randn(8, 4096, device=cuda).half()
+    ref = fpx.gemm_packed(p, x, split_k=4)
+    ws_n = int(L.fpx_linear_workspace_size(p.rows, p.cols, p.cols, 8, 4))
+    ws = torch.zeros(ws_n, dtype=torch.uint8, device=cuda)
+    ws[:4096] = 1  # stale counters
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.fpx_linear_workspace_reset(ws.data_ptr(), ws_n, s) == 0
+    import ctypes as C
+    ptrs = (C.c_void_p * 2)(*[t.data_ptr() for t in p.streams])
+    out = torch.empty_like(ref)
+    assert L.fpx_linear(ptrs, 2, p.scales.data_ptr(), p.rows, p.cols, 3, 2, x.data_ptr(), p.cols, 8, out.data_ptr(),
+                        p.rows, 4, ws.data_ptr(), ws_n, s) == 0
+    assert torch.equal(out, ref)
+    assert int(ws[:65536].count_nonzero()) == 0  # self-cleaned again
+    assert L.fpx_linear_workspace_reset(None, 0, s) == 1 + fpx.ErrorCode.InvalidValue
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck", "racecheck", "initcheck"])
+def test_compute_sanitizer(cuda, tool):
+    """compute-sanitizer over every device entry point at small shapes (K0
+    quantize, fused quantize+pack, K1 prepack / unpack, K3 both de-quantisers,
+    K2 decode and single-issuer kernels at N 1..200 and splits 1/3, ragged
+    K, fused epilogue, sharded helpers): no error reports."""
+    import shutil
+    exe = os.path.join(ROOT, "paper_2401_14112_b200", "build", "fpx_sanitize_driver")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    args = [cs, "--tool", tool, "--error-exitcode", "9"]
+    if tool == "memcheck":
+        args += ["--leak-check", "no"]
+    r = subprocess.run(args + [exe], capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    print(out[-2000:])
+    assert r.returncode == 0 and "sanitize driver ok" in out, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]

@@ -1,6 +1,6 @@
 """Bring-up timing sweep of fpx_linear pipeline variants (GPU box only).
 
-env: KM/KK shape; NS batches; SPLITS; KERNELS (classic,grouped); CFGS
+env: KM/KK shape; NS batches; SPLITS; CFGS
 ("KS,G;..."); VARIANTS (FPX_LINEAR_DBG values: 1 no dequant, 2 no MMA,
 4 no weight loads, 8 no activation loads).  Each timing is 30 back-to-back
 launches over 3 rotated weight copies (405 MB > L2); every configuration is
@@ -66,12 +66,10 @@ def timeit(n, split, iters=30):
 
 variants = os.environ.get("VARIANTS", "0").split(",")
 cfgs = os.environ.get("CFGS", "").split(";") if os.environ.get("CFGS") else [None]
-kernels = os.environ.get("KERNELS", "grouped").split(",")
 splits = [int(x) for x in os.environ.get("SPLITS", "0").split(",")]
 ns = [int(x) for x in os.environ.get("NS", "1,16").split(",")]
 print(f"M={M} K={K} {fmt.name()} weight bytes {wbytes/1e6:.1f} MB", flush=True)
-for kern in kernels:
-    os.environ["FPX_LINEAR_KERNEL"] = kern
+for kern in ["decode"]:
     for cfg in cfgs:
         if cfg:
             os.environ["FPX_LINEAR_CFG"] = cfg

@@ -1,6 +1,6 @@
 """Step-by-step GPU bring-up probe (prints, does not assert).
 
-Run on the GPU box:  timeout 300 python tests/gpu_probe.py
+Run on the GPU box:  timeout 300 python tools/gpu_probe.py
 Each stage compares the sm_100a kernels with the C oracle and prints the
 mismatch statistics, so a failing stage can be diagnosed from one run.
 """
