@@ -17,12 +17,26 @@ e2e    : same sweep through the public API with host buffers: pinned host
          activations -> H2D, fpx_linear, C -> pinned host (D2H) every launch,
          copies on two copy streams pipelined against the launches; packed
          weights stay resident in HBM (loaded once, like a model).
+Beside the headline (N=1 run, informational keys of the same line):
+  us_per_launch_isolated  each launch alone (no programmatic-dependent-launch
+                          predecessor: a spin kernel drains first)
+  cublas_fp16_us          torch F.linear with the fp16 weight (cuBLAS), same
+                          shapes, same graph timing, 2 rotated 360 MB copies
+  sharded                 the column-sharded path (fpx_linear_sharded with
+                          torch's NCCL communicator): kernel / all-gather /
+                          end-to-end us per batch
+  stack70b                BASELINE configs[4]: the LLaMA-70B linear stack (80
+                          layers x QKV, O, gate, up, down; 51.3 GB of FP6)
+                          per batch 1..128 (column-sharded over the ranks)
 --impl reference: the reference's own CPU gemm_packed (oracle/_ref, compiled
          unmodified from /root/reference) on the host cores, same workload.
 
-Multi-GPU (torchrun): weak scaling -- every rank runs the full step on its
-own weights (the path shards by independent output tiles; no data-path
-collective), timings reduced with MAX over ranks.
+Multi-GPU (torchrun, N > 1): the north-star path -- output channels
+column-partitioned across ranks, weak scaling: the layer is (8192 N) x 22016
+and every rank owns 8192 rows of it (= the N=1 workload); a step runs the
+batch sweep through fpx_linear_sharded (shard kernel + NCCL all-gather over
+NVLink + on-device scatter), so every rank ends each linear with the FULL
+output.  Timings are the max over ranks.
 """
 from __future__ import annotations
 
@@ -54,6 +68,8 @@ def parse():
     ap.add_argument("--batches", default=",".join(map(str, BATCHES)))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip isolated / cuBLAS / sharded / stack70b keys")
+    ap.add_argument("--stack-batches", default="1,16,128")
     return ap.parse_args()
 
 
@@ -140,91 +156,317 @@ def peaks():
 
 
 # --------------------------------------------------------------------- ours
-def run_ours(args, rank, world, local):
-    import torch
+class Ctx:
+    """Per-rank device state shared by the measurements."""
 
-    import paper_2401_14112_b200 as fpx
-    from paper_2401_14112_b200 import fpx as F
+    def __init__(self, rank, world, local):
+        import torch
+        self.torch = torch
+        import paper_2401_14112_b200 as fpx
+        self.fpx = fpx
+        self.L = fpx._lib.load()
+        self.rank, self.world, self.local = rank, world, local
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.dist = None
+        self.comm = None
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
+    def init_dist(self):
+        """NCCL process group (torch plumbing); world 1 uses a private store."""
+        if self.dist is not None:
+            return
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    batches = [int(x) for x in args.batches.split(",")]
-    fmt = fpx.FpxFormat.e3m2()
-    L = fpx._lib.load()
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        else:
+            dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1, device_id=self.dev)
+        t = self.torch.ones(1, device=self.dev)
+        dist.all_reduce(t)  # the communicator exists from here on
+        self.dist = dist
+        self.comm = dist.group.WORLD._get_backend(self.dev)._comm_ptr()
 
-    # ---- setup (untimed): synthetic weights, quantize + pack on GPU
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def capture(self, fn):
+        """CUDA graph of fn(): a decode step is ~0.2 ms of device work but ~0.15 ms of
+        host-side ctypes/C-ABI calls, so eager launches would time the host."""
+        torch = self.torch
+        torch.cuda.synchronize(self.dev)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        gr.replay()  # warm
+        torch.cuda.synchronize(self.dev)
+        return gr
+
+    def timed(self, gr, reps=1):
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.barrier()
+        e0.record()
+        for _ in range(reps):
+            gr.replay()
+        e1.record()
+        self.barrier()
+        return e0.elapsed_time(e1)
+
+    def stream(self):
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+
+def make_packed(ctx, rows, cols, seed, fmt=(3, 2)):
+    torch = ctx.torch
+    g = torch.Generator(device=ctx.dev)
+    g.manual_seed(seed)
+    w = torch.randn(rows, cols, device=ctx.dev, generator=g) * 0.02
+    p = ctx.fpx.quantize_pack(w, ctx.fpx.FpxFormat(*fmt))
+    del w
+    return p
+
+
+def clone_packed(ctx, p):
+    return ctx.fpx.PackedWeights(p.format, p.split, p.rows, p.cols, p.orig_rows, p.orig_cols,
+                                 [s.clone() for s in p.streams], p.scales.clone())
+
+
+def measure_isolated(ctx, launch, n, reps=12):
+    """Each launch alone: a ~100 us spin kernel runs first (so the host is
+    ahead and the launch has no programmatic-dependent-launch overlap with a
+    predecessor of its own kind), events bracket just the linear.  Median us."""
+    torch = ctx.torch
+    ts = []
+    for i in range(reps + 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200000)
+        e0.record()
+        launch(i)
+        e1.record()
+        torch.cuda.synchronize(ctx.dev)
+        if i >= 2:
+            ts.append(e0.elapsed_time(e1) * 1e3)
+    return float(np.median(ts))
+
+
+def measure_cublas(ctx, batches, M, K, launches=12):
+    """cuBLAS FP16 (torch F.linear, fp16 in / fp16 out, fp32 accumulate) of the
+    same shape, CUDA-graph timed like ours, 2 rotated fp16 weights (2 x 360 MB)."""
+    torch = ctx.torch
+    g = torch.Generator(device=ctx.dev)
+    g.manual_seed(99)
+    ws = [(torch.randn(M, K, device=ctx.dev, generator=g) * 0.02).half() for _ in range(2)]
+    out = {}
+    for n in batches:
+        x = torch.randn(n, K, device=ctx.dev, generator=g).half()
+        for i in range(3):
+            torch.nn.functional.linear(x, ws[i % 2])
+        gr = ctx.capture(lambda: [torch.nn.functional.linear(x, ws[i % 2]) for i in range(launches)])
+        out[n] = ctx.max_over_ranks(ctx.timed(gr, 2) * 1e3 / (2 * launches))
+    del ws
+    torch.cuda.empty_cache()
+    return out
+
+
+def sharded_launcher(ctx, shard_copies, rows_full, K, split=-1):
+    """fpx_linear_sharded over this rank's shard (rows [8192 r, 8192 (r+1)) of
+    a rows_full x K layer) with torch's NCCL communicator; returns
+    launch(i, n, act_ptr, out_ptr) and the workspace."""
+    import ctypes as C
+    L, torch = ctx.L, ctx.torch
+    ptrs = [(C.c_void_p * 2)(*[s.data_ptr() for s in cp.streams]) for cp in shard_copies]
+    ws_need = max(int(L.fpx_linear_sharded_workspace_size(rows_full, K, K, n, ctx.world, split)) for n in BATCHES)
+    ws = torch.zeros(ws_need, dtype=torch.uint8, device=ctx.dev)
+
+    def launch(i, n, act_ptr, out_ptr):
+        cp = shard_copies[i % len(shard_copies)]
+        st = L.fpx_linear_sharded(ptrs[i % len(shard_copies)], 2, cp.scales.data_ptr(), rows_full, K, 3, 2, act_ptr,
+                                  K, n, out_ptr, rows_full, split, ctx.rank, ctx.world, ctx.comm, ws.data_ptr(),
+                                  ws.numel(), ctx.stream())
+        if st:
+            raise RuntimeError(L.fpx_last_error().decode())
+
+    return launch, ws
+
+
+def measure_sharded(ctx, shard_copies, rows_full, K, batches, launches=12):
+    """Per batch: the shard kernel alone, the NCCL all-gather of the output
+    slices alone, and the whole fpx_linear_sharded call (us, max over ranks)."""
+    import ctypes as C
+    torch, L = ctx.torch, ctx.L
+    launch, ws = sharded_launcher(ctx, shard_copies, rows_full, K)
+    m_local = shard_copies[0].rows
+    ptrs = [(C.c_void_p * 2)(*[s.data_ptr() for s in cp.streams]) for cp in shard_copies]
+    res = {}
+    for n in batches:
+        act = torch.randn(n, K, device=ctx.dev).half()
+        out = torch.empty(n, rows_full, device=ctx.dev)
+        loc = torch.empty(n, m_local, device=ctx.dev)
+        split = int(L.fpx_linear_default_split(m_local, K, n))
+        lws_n = int(L.fpx_linear_workspace_size(m_local, K, K, n, split))
+        lws = torch.zeros(lws_n, dtype=torch.uint8, device=ctx.dev)
+
+        def kern(i):
+            cp = shard_copies[i % len(shard_copies)]
+            st = L.fpx_linear(ptrs[i % len(shard_copies)], 2, cp.scales.data_ptr(), m_local, K, 3, 2, act.data_ptr(),
+                              K, n, loc.data_ptr(), m_local, split, lws.data_ptr(), lws_n, ctx.stream())
+            assert st == 0, L.fpx_last_error()
+
+        gathered = torch.empty(ctx.world * n * m_local, device=ctx.dev)
+        flat = loc.view(-1)
+
+        def gather(i):
+            ctx.dist.all_gather_into_tensor(gathered, flat)
+
+        def gather_us():
+            """NCCL all-gather alone (graph-captured when the process group
+            allows it, else eager with events)."""
+            try:
+                for i in range(3):
+                    gather(i)
+                gr = ctx.capture(lambda: [gather(i) for i in range(launches)])
+                return ctx.timed(gr, 2) * 1e3 / (2 * launches)
+            except Exception:  # noqa: BLE001
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ctx.barrier()
+                e0.record()
+                for i in range(launches):
+                    gather(i)
+                e1.record()
+                ctx.barrier()
+                return e0.elapsed_time(e1) * 1e3 / launches
+
+        r = {}
+        for name, fn in (("kernel_us", kern), ("e2e_us", lambda i: launch(i, n, act.data_ptr(), out.data_ptr()))):
+            for i in range(3):
+                fn(i)
+            gr = ctx.capture(lambda: [fn(i) for i in range(launches)])
+            r[name] = round(ctx.max_over_ranks(ctx.timed(gr, 2) * 1e3 / (2 * launches)), 2)
+        r["allgather_us"] = round(ctx.max_over_ranks(gather_us()), 2)
+        r["split"] = split
+        res[n] = r
+    return res
+
+
+STACK70B = (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate", 28672, 8192), ("up", 28672, 8192),
+            ("down", 8192, 28672))
+
+
+def measure_stack70b(ctx, batches, layers=80):
+    """BASELINE configs[4]: the LLaMA-70B decoder linear stack, 80 layers x
+    (QKV, O, gate, up, down), FP6 e3m2, column-sharded over the ranks (rank r
+    holds tile-rows fpx_shard_rows(M, r, world) of every linear: 51.3 GB / world
+    of packed weights).  One pass = the 400 linears in order, each on the batch
+    and -- at world > 1 -- followed by the NCCL all-gather of its output
+    (fpx_linear_sharded, shard-local split); at world 1 plain fpx_linear.
+    Timed as one CUDA graph per batch.  Weight GB/s counts the full stack."""
+    import ctypes as C
+    torch, L, fpx = ctx.torch, ctx.L, ctx.fpx
+    import math
+    from paper_2401_14112_b200 import shard
+    t0 = time.time()
+    packs = []  # [layer][linear] -> (PackedWeights shard, ptr array)
+    for layer in range(layers):
+        row = []
+        for j, (_, M, K) in enumerate(STACK70B):
+            tr0, tr1 = shard.shard_tile_rows(M, ctx.rank, ctx.world)
+            p = make_packed(ctx, (tr1 - tr0) * 64, K, seed=7000 + 10 * layer + j + 100000 * ctx.rank)
+            row.append((p, (C.c_void_p * 2)(*[s.data_ptr() for s in p.streams])))
+        packs.append(row)
+    torch.cuda.synchronize(ctx.dev)
+    setup_s = time.time() - t0
+    full_bytes = layers * sum(M * K * 6 // 8 for _, M, K in STACK70B)
+    res = {}
+    nmax = max(batches)
+    acts = {K: torch.randn(nmax, K, device=ctx.dev).half() for K in (8192, 28672)}
+    outs = {M: torch.empty(nmax, M, device=ctx.dev) for _, M, _ in STACK70B}
+    ws = torch.zeros(256 << 20, dtype=torch.uint8, device=ctx.dev)
+    for n in batches:
+        if ctx.world == 1:
+            def one(p, ptrs, M, K):
+                st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
+                                  outs[M].data_ptr(), M, 0, ws.data_ptr(), ws.numel(), ctx.stream())
+                assert st == 0, L.fpx_last_error()
+        else:
+            def one(p, ptrs, M, K):
+                st = L.fpx_linear_sharded(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
+                                          outs[M].data_ptr(), M, -1, ctx.rank, ctx.world, ctx.comm, ws.data_ptr(),
+                                          ws.numel(), ctx.stream())
+                assert st == 0, L.fpx_last_error()
+
+        def stack_pass():
+            for row in packs:
+                for (p, ptrs), (_, M, K) in zip(row, STACK70B):
+                    one(p, ptrs, M, K)
+
+        stack_pass()
+        gr = ctx.capture(stack_pass)
+        ms = ctx.max_over_ranks(ctx.timed(gr, 2) / 2)
+        res[str(n)] = {"ms": round(ms, 3), "weight_GBps": round(full_bytes / (ms * 1e-3) / 1e9, 1),
+                       "TFLOPs": round(2.0 * full_bytes * 8 / 6 * n / (ms * 1e-3) / 1e12, 1)}
+        del gr
+    del packs
+    torch.cuda.empty_cache()
+    return {"layers": layers, "linears": [f"{nm} {M}x{K}" for nm, M, K in STACK70B],
+            "weight_bytes": full_bytes, "world": ctx.world,
+            "sharding": "column (output rows) per rank + NCCL all-gather per linear" if ctx.world > 1 else "1 GPU",
+            "setup_s": round(setup_s, 1), "per_batch": res,
+            "timing": "one CUDA graph of the 400 linears per batch, 2 replays, max over ranks"}
+
+
+def run_ours(args, rank, world, local):
+    import ctypes as C
+    ctx = Ctx(rank, world, local)
+    torch, fpx, L, dev = ctx.torch, ctx.fpx, ctx.L, ctx.dev
+    if world > 1:
+        ctx.init_dist()
+    batches = [int(x) for x in args.batches.split(",")]
+
+    # ---- setup (untimed): synthetic weights, quantize + pack on GPU.  At
+    # world > 1 this rank's 8192 x 22016 block is its shard of the
+    # (8192 world) x 22016 column-partitioned layer.
+    fmt = fpx.FpxFormat.e3m2()
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     w = torch.randn(M_ROWS, K_COLS, device=dev, generator=g) * 0.02
     q = fpx.quantize_matrix(w, fmt)
     packed = fpx.pack(q)
-    codes_host = q.codes.cpu().numpy() if (rank == 0 and not args.no_cpu_baseline) else None
+    codes_host = q.codes.cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     scales_host = q.scales.cpu().numpy().view(np.uint16) if codes_host is not None else None
     del w, q
     n_copies = 3
-    copies = [packed] + [fpx.PackedWeights(packed.format, packed.split, packed.rows, packed.cols, packed.orig_rows,
-                                           packed.orig_cols, [s.clone() for s in packed.streams],
-                                           packed.scales.clone()) for _ in range(n_copies - 1)]
+    copies = [packed] + [clone_packed(ctx, packed) for _ in range(n_copies - 1)]
+    rows_out = M_ROWS * world
     acts = {n: (torch.randn(n, K_COLS, device=dev, generator=g)).half() for n in batches}
-    outs = {n: torch.empty(n, M_ROWS, device=dev) for n in batches}
+    outs = {n: torch.empty(n, rows_out, device=dev) for n in batches}
     splits = {n: fpx.default_split(M_ROWS, K_COLS, n) for n in batches}
     ws_need = max(int(L.fpx_linear_workspace_size(M_ROWS, K_COLS, K_COLS, n, splits[n])) for n in batches)
     ws = torch.zeros(ws_need, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    import ctypes as C
     ptrs = [(C.c_void_p * 2)(*[s.data_ptr() for s in cp.streams]) for cp in copies]
 
-    def launch(i, n, act_ptr, out_ptr):
-        cp = copies[i % n_copies]
-        st = L.fpx_linear(ptrs[i % n_copies], 2, cp.scales.data_ptr(), M_ROWS, K_COLS, 3, 2, act_ptr, K_COLS, n,
-                          out_ptr, M_ROWS, splits[n], ws.data_ptr(), ws.numel(),
-                          torch.cuda.current_stream(dev).cuda_stream)
-        if st:
-            raise RuntimeError(L.fpx_last_error().decode())
+    if world == 1:
+        def launch(i, n, act_ptr, out_ptr):
+            cp = copies[i % n_copies]
+            st = L.fpx_linear(ptrs[i % n_copies], 2, cp.scales.data_ptr(), M_ROWS, K_COLS, 3, 2, act_ptr, K_COLS, n,
+                              out_ptr, M_ROWS, splits[n], ws.data_ptr(), ws.numel(), ctx.stream())
+            if st:
+                raise RuntimeError(L.fpx_last_error().decode())
+    else:
+        launch, _sws = sharded_launcher(ctx, copies, rows_out, K_COLS, split=-1)
 
     def step(counter):
         for n in batches:
             launch(counter, n, acts[n].data_ptr(), outs[n].data_ptr())
             counter += 1
         return counter
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def capture(fn):
-        """CUDA graph of fn(): a decode step is ~0.2 ms of device work but ~0.15 ms of
-        host-side ctypes/C-ABI calls, so eager launches would time the host."""
-        torch.cuda.synchronize(dev)
-        gr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gr):
-            fn()
-        gr.replay()  # warm
-        torch.cuda.synchronize(dev)
-        return gr
-
-    def timed(gr, reps=1):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        e0.record()
-        for _ in range(reps):
-            gr.replay()
-        e1.record()
-        barrier()
-        return e0.elapsed_time(e1)
 
     cnt = 0
     for _ in range(args.warmup):
@@ -237,20 +479,19 @@ def run_ours(args, rank, world, local):
         for _ in range(args.steps):
             c = step(c)
 
-    # per-batch device time of the fused kernel (informational: graph of 12
-    # launches per N, 3 weight copies rotated), measured before the timed
-    # region and its clock soak
+    # per-batch device time (informational: graph of 12 launches per N, 3
+    # weight copies rotated), measured before the timed region and its soak
     per_n = {}
     for n in batches:
-        gr = capture(lambda: [launch(i, n, acts[n].data_ptr(), outs[n].data_ptr()) for i in range(12)])
-        per_n[n] = max_over_ranks(timed(gr, 2) * 1e3 / 24)  # us per launch
+        gr = ctx.capture(lambda: [launch(i, n, acts[n].data_ptr(), outs[n].data_ptr()) for i in range(12)])
+        per_n[n] = ctx.max_over_ranks(ctx.timed(gr, 2) * 1e3 / 24)  # us per launch
 
-    g_steps = capture(k_steps)
+    g_steps = ctx.capture(k_steps)
     for _ in range(args.warmup):  # warm-up replays of the timed graph itself
         g_steps.replay()
-    barrier()
+    ctx.barrier()
     with ClockSampler(local) as clk:
-        total_ms = max_over_ranks(timed(g_steps))
+        total_ms = ctx.max_over_ranks(ctx.timed(g_steps))
         # The timed region lasts a few ms, below nvidia-smi's sampling period:
         # keep replaying the identical steps (untimed) for >= 0.3 s so the
         # clock/throttle samples describe this workload under load.
@@ -258,7 +499,7 @@ def run_ours(args, rank, world, local):
         while time.time() < soak_end:
             g_steps.replay()
             torch.cuda.synchronize(dev)
-
+    del g_steps
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -267,7 +508,7 @@ def run_ours(args, rank, world, local):
         # ONE device block, and so do its outputs: one H2D and one D2H per step
         # (each small cudaMemcpy costs several us of copy-engine time).
         tot_a = sum(n * K_COLS for n in batches)
-        tot_c = sum(n * M_ROWS for n in batches)
+        tot_c = sum(n * rows_out for n in batches)
         h_act_all = torch.cat([acts[n].reshape(-1) for n in batches]).cpu().pin_memory()
         h_out_all = torch.empty(tot_c, pin_memory=True)
 
@@ -282,7 +523,7 @@ def run_ours(args, rank, world, local):
         d_act_all = [torch.empty(tot_a, dtype=torch.float16, device=dev) for _ in range(2)]
         d_out_all = [torch.empty(tot_c, dtype=torch.float32, device=dev) for _ in range(2)]
         d_act = [views(b, K_COLS) for b in d_act_all]
-        d_out = [views(b, M_ROWS) for b in d_out_all]
+        d_out = [views(b, rows_out) for b in d_out_all]
         s_h2d = torch.cuda.Stream(dev)
         s_d2h = torch.cuda.Stream(dev)
 
@@ -328,25 +569,49 @@ def run_ours(args, rank, world, local):
             main.wait_event(j1)
             main.wait_event(j2)
 
-        g_e2e = capture(e2e_steps)
-        e2e_ms = max_over_ranks(timed(g_e2e))
+        g_e2e = ctx.capture(e2e_steps)
+        e2e_ms = ctx.max_over_ranks(ctx.timed(g_e2e))
+        del g_e2e
         h2d = tot_a * 2
         d2h = tot_c * 4
         e2e = {"value": round(world * nl * WEIGHT_BYTES / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(e2e_ms / args.steps, 4),
                "note": "per step: one H2D of the six batches' pinned host activations (copy stream) + the six "
-                       "fpx_linear calls (C-ABI, compute stream) + one D2H of their fp32 outputs (second copy stream), "
-                       "double-buffered so copies overlap the neighbouring steps' launches; replayed as one CUDA "
-                       "graph; packed weights resident in HBM"}
+                       + ("fpx_linear_sharded calls (C-ABI: shard kernel + NCCL all-gather + scatter, compute stream)"
+                          if world > 1 else "fpx_linear calls (C-ABI, compute stream)")
+                       + " + one D2H of their fp32 outputs (second copy stream), double-buffered so copies overlap "
+                         "the neighbouring steps' launches; replayed as one CUDA graph; packed weights resident in "
+                         "HBM"}
 
-    # ---- correctness spot check (untimed): last outputs vs a dequant+matmul
+    # ---- correctness spot check (untimed): this rank's output rows vs a dequant+matmul
     W16 = fpx.dequantize(copies[0]).float()
     n_chk = batches[-1]
     ref = acts[n_chk].float() @ W16.t()
-    got = fpx.gemm_packed(copies[0], acts[n_chk], split_k=splits[n_chk])
+    launch(0, n_chk, acts[n_chk].data_ptr(), outs[n_chk].data_ptr())
+    got = outs[n_chk][:, rank * M_ROWS:(rank + 1) * M_ROWS]
     rel = float(((got - ref).abs().amax(dim=1) / ref.abs().amax(dim=1)).max())
     del W16, ref
+
+    extras = {}
+    if not args.no_extras:
+        extras["us_per_launch_isolated"] = {
+            str(n): round(ctx.max_over_ranks(measure_isolated(
+                ctx, lambda i, n=n: launch(i, n, acts[n].data_ptr(), outs[n].data_ptr()), n)), 2) for n in batches}
+        cub = measure_cublas(ctx, batches, M_ROWS, K_COLS)
+        extras["cublas_fp16_us"] = {str(n): round(v, 2) for n, v in cub.items()}
+        extras["speedup_vs_cublas_fp16"] = {str(n): round(cub[n] / per_n[n], 2) for n in batches}
+        if world == 1:
+            ctx.init_dist()
+            extras["sharded"] = {"world": 1, "per_batch": {str(n): v for n, v in measure_sharded(
+                ctx, copies, M_ROWS, K_COLS, batches).items()},
+                "note": "fpx_linear_sharded through torch's NCCL communicator (1 rank): kernel = the shard's fused "
+                        "linear alone, allgather = ncclAllGather of the output slices alone, e2e = the whole call"}
+        del copies, packed
+        torch.cuda.empty_cache()
+        sb = [int(x) for x in args.stack_batches.split(",") if x]
+        if sb:
+            extras["stack70b"] = measure_stack70b(ctx, sb)
 
     hbm, hbm_src = peaks()
     traffic, traffic_src = ncu_traffic()
@@ -355,15 +620,22 @@ def run_ours(args, rank, world, local):
     # its mean launch duration is the kernel's, measured live on its stream
     mean_launch_us = total_ms * 1e3 / nl
     achieved = WEIGHT_BYTES / (mean_launch_us * 1e-6) / 1e9
+    if world == 1:
+        workload = ("llama-65B FFN linear 8192x22016 FP6 e3m2, batch sweep 1/2/4/8/16/32 (one fused linear per "
+                    "batch per step)")
+        par = "x1"
+    else:
+        workload = (f"llama-65B FFN linear column-sharded: a ({M_ROWS}x{world})x{K_COLS} FP6 e3m2 layer, {M_ROWS} "
+                    f"rows per rank, batch sweep 1/2/4/8/16/32, every linear all-gathered (fpx_linear_sharded)")
+        par = f"column-sharded x{world} (NCCL all-gather of outputs)"
     res = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp6(e3m2) weights x fp16 activations -> fp32 (f16 MMA)",
         "data": "synthetic: N(0,0.02) weights quantized/packed on GPU, N(0,1) fp16 activations",
-        "config": {"workload": "llama-65B FFN linear 8192x22016 FP6 e3m2, batch sweep 1/2/4/8/16/32 (one fused "
-                               "linear per batch per step)", "M": M_ROWS, "K": K_COLS, "batches": batches,
-                   "split_k": splits, "l2": "3 rotated packed-weight copies (405 MB > 126 MB L2)",
-                   "parallelism": f"weak x{world} (independent output tiles per rank)"},
+        "config": {"workload": workload, "M": M_ROWS, "K": K_COLS, "batches": batches,
+                   "split_k": splits if world == 1 else "shard-local (fpx_linear_sharded split -1)",
+                   "l2": "3 rotated packed-weight copies (405 MB > 126 MB L2)", "parallelism": par},
         "us_per_launch": {str(n): round(v, 2) for n, v in per_n.items()},
         "timing": "CUDA events around CUDA-graph replays of the K timed steps (host launch overhead excluded)",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -371,19 +643,20 @@ def run_ours(args, rank, world, local):
                      "traffic_source": f"{traffic_src} (N=16 launch, dram read+write bytes)" if traffic else None,
                      "peak_source": f"{hbm_src} MEASURED_PEAKS.json hbm_gbs" if hbm_src == "measured" else hbm_src,
                      "kernel": "fpx_linear_decode_kernel (mean device time per launch over the timed region: "
-                               "K steps x the batch sweep, back to back)",
+                               "K steps x the batch sweep, back to back)" + (
+                                   "; includes the all-gather" if world > 1 else ""),
                      "us_per_launch": round(mean_launch_us, 2),
                      "algorithmic_bytes_per_launch": WEIGHT_BYTES},
-        "gpu_launches": nl,  # one fused kernel per batch per step
+        "gpu_launches": nl * (2 if world > 1 else 1),  # fused kernel (+ scatter kernel when sharded) per batch per step
         "clocks": clk.summary(),
         "e2e": e2e,
         "check": {"max_rel_err_vs_dequant_matmul": rel, "tol": 1e-2},
     }
+    res.update(extras)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         res["cpu_baseline"] = cpu_baseline(codes_host, scales_host, batches, sample_batches=batches)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    if ctx.dist is not None:
+        ctx.dist.destroy_process_group()
     return res
 
 

@@ -190,12 +190,18 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
  * `world` holds tile-rows fpx_shard_rows(rows_p, rank, world) of the packed
  * weight (shard_streams / shard_scales = that contiguous byte range, zero
  * copy); every rank passes the same activations and receives the FULL
- * col-major C (rows_p x n, ldc).  The shard runs with the full problem's
- * split_k (0 -> fpx_linear_default_split(rows_p, cols_p, n)), so its rows are
- * bit-identical to a 1-GPU call; the slices are all-gathered over NVLink
- * with ncclAllGather on `stream` (nccl_comm: the caller's ncclComm_t, from
- * the NCCL already loaded in the process -- resolved at run time, no link
- * dependency) and scattered into C.  world == 1 needs no communicator. */
+ * col-major C (rows_p x n, ldc).  split_k 0 runs the shard with the full
+ * problem's split (fpx_linear_default_split(rows_p, cols_p, n)), so its rows
+ * are bit-identical to a 1-GPU call; -1 picks the split that suits the shard
+ * (the per-rank default; within the usual tolerance of a 1-GPU call, and
+ * what scales: the full problem's split can leave most SMs of a small shard
+ * idle); > 0 is used as given.  The slices are all-gathered over NVLink
+ * with ncclAllGather on `stream` (nccl_comm: the caller's ncclComm_t) and
+ * scattered into C.  NCCL is resolved at run time, no link dependency:
+ * FPX_NCCL_LIB if set, else the one libnccl already mapped into the process
+ * (e.g. torch's), else libnccl.so.2; two different libnccl files mapped at
+ * once is refused (FPX_ERR_DEVICE) rather than guessed.  world == 1 needs
+ * no communicator. */
 size_t fpx_linear_sharded_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int world,
                                          int split_k);
 int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint16_t* shard_scales, uint32_t rows_p,

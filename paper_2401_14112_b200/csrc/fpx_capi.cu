@@ -4,6 +4,7 @@
 // no host compute fallback: if the device or a kernel is unavailable the
 // call fails with FPX_ERR_DEVICE / FPX_ERR_CUDA.
 #include <dlfcn.h>
+#include <link.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -631,20 +632,57 @@ int fpx_gather_permute(const float* gathered, const uint32_t* row0, const uint32
 }
 
 // ---------------------------------------------------------------- sharded linear
-// NCCL is resolved at call time from the process (dlsym RTLD_DEFAULT, e.g.
-// torch's NCCL), else libnccl.so.2: the ncclComm_t the caller passes must
-// come from the very library whose ncclAllGather runs, and libfpx_b200.so
-// carries no link-time NCCL dependency.
+// NCCL is resolved at call time, never linked: the ncclComm_t the caller
+// passes must come from the very library whose ncclAllGather runs.  The
+// library is (1) FPX_NCCL_LIB when set, else (2) the one libnccl already
+// mapped into the process (e.g. torch's), else (3) libnccl.so.2 from the
+// loader path.  Two different libnccl files mapped at once is ambiguous --
+// a communicator from one is garbage to the other -- and fails loudly.
+struct NcclScan {
+    std::string paths[4];
+    int n = 0;
+};
+
+static int nccl_scan_cb(struct dl_phdr_info* info, size_t, void* data) {
+    auto* sc = static_cast<NcclScan*>(data);
+    const char* name = info->dlpi_name;
+    if (name == nullptr || std::strstr(name, "libnccl") == nullptr) return 0;
+    for (int i = 0; i < sc->n; ++i)
+        if (sc->paths[i] == name) return 0;
+    if (sc->n < 4) sc->paths[sc->n++] = name;
+    return 0;
+}
+
 typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
-static nccl_allgather_fn nccl_allgather() {
-    static nccl_allgather_fn fn = [] {
-        void* f = dlsym(RTLD_DEFAULT, "ncclAllGather");
-        if (f == nullptr) {
-            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-            if (h != nullptr) f = dlsym(h, "ncclAllGather");
+static nccl_allgather_fn nccl_allgather(std::string* why) {
+    static std::mutex mu;
+    static nccl_allgather_fn fn = nullptr;
+    static std::string err;
+    std::lock_guard<std::mutex> lk(mu);
+    if (fn != nullptr) return fn;
+    void* h = nullptr;
+    if (const char* env = std::getenv("FPX_NCCL_LIB")) {
+        h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) err = std::string("FPX_NCCL_LIB ") + env + ": " + dlerror();
+    } else {
+        NcclScan sc;
+        dl_iterate_phdr(nccl_scan_cb, &sc);
+        if (sc.n > 1) {
+            err = "two NCCL libraries are loaded (" + sc.paths[0] + ", " + sc.paths[1] +
+                  "); set FPX_NCCL_LIB to the one that created the communicator";
+        } else if (sc.n == 1) {
+            h = dlopen(sc.paths[0].c_str(), RTLD_NOW | RTLD_NOLOAD);
+            if (h == nullptr) err = "cannot re-open " + sc.paths[0];
+        } else {
+            h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (h == nullptr) err = "libnccl.so.2 not found (load NCCL first)";
         }
-        return reinterpret_cast<nccl_allgather_fn>(f);
-    }();
+    }
+    if (h != nullptr) {
+        fn = reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather"));
+        if (fn == nullptr) err = "ncclAllGather not exported by the NCCL library";
+    }
+    if (why) *why = err;
     return fn;
 }
 
@@ -656,8 +694,9 @@ static uint32_t shard_slot_rows(uint32_t rows_p, int world) {
 size_t fpx_linear_sharded_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_act, uint32_t n, int world,
                                          int split_k) {
     if (world <= 0) world = 1;
-    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
     const uint32_t slot = shard_slot_rows(rows_p, world);
+    if (split_k == -1) split_k = fpx_linear_default_split(slot, cols_p, n);
+    if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
     const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
     return lin + align256(size_t(slot) * n * 4) + align256(size_t(world) * slot * n * 4);
 }
@@ -671,16 +710,20 @@ int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint
     if (ldc < rows_p) return fail(FPX_ERR_SHAPE_MISMATCH, "ldc %u < rows %u", ldc, rows_p);
     if (n == 0) return FPX_OK;
     if (world > 1 && nccl_comm == nullptr) return fail(FPX_ERR_INVALID_VALUE, "world > 1 needs an NCCL communicator");
-    nccl_allgather_fn ag = world > 1 ? nccl_allgather() : nullptr;
-    if (world > 1 && ag == nullptr) return fail(FPX_ERR_DEVICE, "ncclAllGather not found (load NCCL first)");
-    // the FULL problem's split: shard rows are bit-identical to a 1-GPU run
+    std::string why;
+    nccl_allgather_fn ag = world > 1 ? nccl_allgather(&why) : nullptr;
+    if (world > 1 && ag == nullptr) return fail(FPX_ERR_DEVICE, "%s", why.c_str());
+    uint32_t tr0 = 0, tr1 = 0;
+    fpx_shard_rows(rows_p, rank, world, &tr0, &tr1);
+    const uint32_t slot = shard_slot_rows(rows_p, world), m_local = (tr1 - tr0) * 64u;
+    // 0: the FULL problem's split -- shard rows bit-identical to a 1-GPU run;
+    // -1: the split that suits this shard (every rank's rows are computed
+    // identically for a given world size, within the tolerance of a 1-GPU run).
+    if (split_k == -1) split_k = fpx_linear_default_split(slot, cols_p, n);
     if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
     const size_t need = fpx_linear_sharded_workspace_size(rows_p, cols_p, k_act, n, world, split_k);
     if (workspace == nullptr || workspace_bytes < need)
         return fail(FPX_ERR_INVALID_VALUE, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
-    uint32_t tr0 = 0, tr1 = 0;
-    fpx_shard_rows(rows_p, rank, world, &tr0, &tr1);
-    const uint32_t slot = shard_slot_rows(rows_p, world), m_local = (tr1 - tr0) * 64u;
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
     float* local = reinterpret_cast<float*>(ws + lin);
@@ -695,8 +738,7 @@ int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint
         FPX_CUDA(launch_gather_shards(local, rows_p, 1, slot, n, c, ldc, s));
         return FPX_OK;
     }
-    if (ag == nullptr && (ag = nccl_allgather()) == nullptr)
-        return fail(FPX_ERR_DEVICE, "ncclAllGather not found (load NCCL first)");
+    if (ag == nullptr && (ag = nccl_allgather(&why)) == nullptr) return fail(FPX_ERR_DEVICE, "%s", why.c_str());
     const int nst = ag(local, gathered, size_t(slot) * n, /*ncclFloat32*/ 7, nccl_comm, s);
     if (nst != 0) return fail(FPX_ERR_CUDA, "ncclAllGather failed (ncclResult %d)", nst);
     FPX_CUDA(launch_gather_shards(gathered, rows_p, world, slot, n, c, ldc, s));

@@ -426,7 +426,13 @@ __global__ void __launch_bounds__(256) dequant_codes_kernel(const uint8_t* __res
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const uint4 cw = __ldcs(reinterpret_cast<const uint4*>(codes) + i);
         const size_t row = i / vec_per_row;
-        const __half2 s2 = __half2half2(__ushort_as_half(__ldg(&scales[row])));
+        const uint16_t sraw = __ldg(&scales[row]);
+        const __half2 s2 = __half2half2(__ushort_as_half(sraw));
+        // NaN results follow the reference's host arithmetic (fp32 product on
+        // x86, half.cpp:68-70): a NaN scale propagates quieted with its sign
+        // and payload; inf x 0 is the default NaN 0xFE00.  (Only reachable
+        // with hand-made non-finite scales: quantize never produces them.)
+        const uint32_t nan_fix = (sraw & 0x7fffu) > 0x7c00u ? (sraw | 0x0200u) : 0xfe00u;
         const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
         uint32_t o[8];
         uint32_t any_bad = 0;
@@ -440,7 +446,10 @@ __global__ void __launch_bounds__(256) dequant_codes_kernel(const uint8_t* __res
                 const __half2 d = __halves2half2(__ushort_as_half(static_cast<uint16_t>(lo)),
                                                  __ushort_as_half(static_cast<uint16_t>(hi)));
                 const __half2 r = __hmul2_rn(d, s2);  // fp16 RNE product, subnormals kept (half.cpp:68-70)
-                o[2 * wi + hp] = *reinterpret_cast<const uint32_t*>(&r);
+                uint32_t v = *reinterpret_cast<const uint32_t*>(&r);
+                if ((v & 0x7fffu) > 0x7c00u) v = (v & 0xffff0000u) | nan_fix;
+                if (((v >> 16) & 0x7fffu) > 0x7c00u) v = (v & 0xffffu) | (nan_fix << 16);
+                o[2 * wi + hp] = v;
             }
         }
         if (any_bad) atomicMin(status, (static_cast<unsigned long long>(row) << 8) | 2ull /* FPX_ERR_INVALID_CODE */);
