@@ -275,7 +275,8 @@ __device__ __forceinline__ void dequant_ktile(uint32_t hi, uint32_t lo, int h, u
 
 template <int F, int NPAD, int KS_, int NG_>
 __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
-    fpx_linear_kernel(const __grid_constant__ CUtensorMap act_map, const KParams p) {
+    fpx_linear_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap hi_map,
+                      const __grid_constant__ CUtensorMap lo_map, const KParams p) {
     using C = Cfg<F, NPAD, KS_, NG_>;
     constexpr int KS = C::kKS;
     extern __shared__ uint8_t smem_raw[];
@@ -295,9 +296,12 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
     const uint32_t u_begin = static_cast<uint32_t>((uint64_t)blockIdx.x * p.units / gridDim.x);
     const uint32_t u_end = static_cast<uint32_t>((uint64_t)(blockIdx.x + 1) * p.units / gridDim.x);
 
-    if (warp == C::kProdWarp && lane == 0) prefetch_tmap(&act_map);
+    if (warp == C::kProdWarp && lane == 0) prefetch_tmap(&act_map), prefetch_tmap(&hi_map), prefetch_tmap(&lo_map);
     if (warp == C::kMmaWarp && lane == 0) {
-        for (int i = 0; i < C::kStages; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
+        // empty: the MMA commit (B operand read) + the group's 4 warps (packed
+        // words read), so every reader of the slot arrives before the producer
+        // overwrites it (a thread-visible chain compute-sanitizer can follow)
+        for (int i = 0; i < C::kStages; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 5);
         for (int i = 0; i < C::kAStages; ++i) mbar_init(&afull[i], 4), mbar_init(&aempty[i], 1);
         for (int i = 0; i < 2; ++i) mbar_init(&accfull[i], 1), mbar_init(&accempty[i], 4);
         fence_mbar_init();
@@ -329,29 +333,22 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
             for (uint32_t u = u_begin; u < u_end; ++u) {
                 uint32_t mt, ch, k0, k1;
                 unit_range(p, u, mt, ch, k0, k1);
-                const uint32_t tr0 = 2 * mt;
-                const uint32_t ntr = min(2u, p.tile_rows - tr0);
+                const int32_t tr0 = static_cast<int32_t>(2 * mt);
                 for (uint32_t k = k0; k < k1; k += KS, ++si) {
-                    const uint32_t cnt = min(static_cast<uint32_t>(KS), k1 - k);
                     const uint32_t st = si % C::kStages, ph = (si / C::kStages) & 1u;
                     mbar_wait(&empty[st], ph ^ 1u);
                     trace_mark(p, kTrProdIssue, si);
                     uint8_t* sb = smem + st * C::kStageBytes;
+                    // 3-D boxes {64w, KS, 2}: KS k-tiles of both tile-rows, landing
+                    // [tile-row][k-tile][512w B]; a missing second tile-row and
+                    // k-tiles past the chunk end (KS > 1) are zero-filled / unused
                     const uint32_t bytes = ((p.dbg & 8u) ? 0u : KS * C::kBBytes) +
-                                           ((p.dbg & 4u) ? 0u : ntr * cnt * (C::kHiBytes + C::kLoBytes));
+                                           ((p.dbg & 4u) ? 0u : 2u * KS * (C::kHiBytes + C::kLoBytes));
                     mbar_arrive_expect_tx(&full[st], bytes);
                     if (!(p.dbg & 8u)) tma_load_3d(sb, &act_map, 0, 0, static_cast<int32_t>(k), &full[st], pol_b);
                     if (!(p.dbg & 4u)) {
-                        const size_t tile = static_cast<size_t>(tr0) * p.kt + k;
-                        bulk_g2s(sb + C::kHiOff, p.s_hi + tile * C::kHiBytes, cnt * C::kHiBytes, &full[st], pol_w);
-                        bulk_g2s(sb + C::kLoOff, p.s_lo + tile * C::kLoBytes, cnt * C::kLoBytes, &full[st], pol_w);
-                        if (ntr > 1) {
-                            const size_t tile1 = tile + p.kt;
-                            bulk_g2s(sb + C::kHiOff + KS * C::kHiBytes, p.s_hi + tile1 * C::kHiBytes,
-                                     cnt * C::kHiBytes, &full[st], pol_w);
-                            bulk_g2s(sb + C::kLoOff + KS * C::kLoBytes, p.s_lo + tile1 * C::kLoBytes,
-                                     cnt * C::kLoBytes, &full[st], pol_w);
-                        }
+                        tma_load_3d(sb + C::kHiOff, &hi_map, 0, static_cast<int32_t>(k), tr0, &full[st], pol_w);
+                        tma_load_3d(sb + C::kLoOff, &lo_map, 0, static_cast<int32_t>(k), tr0, &full[st], pol_w);
                     }
                 }
             }
@@ -518,7 +515,7 @@ __global__ void __launch_bounds__(Cfg<F, NPAD, KS_, NG_>::kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) trace_mark(p, q == 0 ? kTrDqDone : kTrDqDone1 + q - 1, si);
-                if (lane == 0) mbar_arrive(&afull[as]);
+                if (lane == 0) mbar_arrive(&afull[as]), mbar_arrive(&empty[st]);
             }
         }
     }
@@ -760,6 +757,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
     const uint32_t lane = lane_id();
     const uint32_t u_begin = static_cast<uint32_t>((uint64_t)blockIdx.x * p.units / gridDim.x);
     const uint32_t u_end = static_cast<uint32_t>((uint64_t)(blockIdx.x + 1) * p.units / gridDim.x);
+    if (threadIdx.x == 0) trace_cta(p, 15);  // kernel entry, before the prologue
 
     if (warp == C::kEpiWarp0 && lane == 0) {
         for (int i = 0; i < SW; ++i) mbar_init(&wfull[i], 1), mbar_init(&wempty[i], 4);
@@ -988,11 +986,9 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             if (p.split > 1) {
                 __threadfence();
                 __syncwarp();
-                if (q == 0 && lane == 0) trace_cta(p, 14);
                 uint32_t old = 0;
                 if (lane == 0) old = atomicAdd(&p.counters[mt * 4 + q], 1u);
                 old = __shfl_sync(0xffffffffu, old, 0);
-                if (q == 0 && lane == 0) trace_cta(p, 15);
                 if (old == p.split - 1 && u + 1 == u_end) {
                     // The CTA's last unit: its reduction would sit on the launch's
                     // tail with 128 threads and one L2 round trip per 4-column
@@ -1100,6 +1096,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     if (q == 0 && lane == 0) trace_mark(p, kTrDqAempty, si);
                     wait_rec(p, &wfull[ws], (si / SW) & 1u, 3, si);
                     if (q == 0 && lane == 0) trace_mark(p, kTrDqFull, si);
+                    if (warp == 0 && lane == 0 && si == 0) trace_cta(p, 14);  // first weight stage landed
                     // all of the stage's packed words into registers, then hand the
                     // weight stage back to the producers
                     uint32_t w[KS][12];
@@ -1267,13 +1264,18 @@ cudaError_t launch_t(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
     auto kern = fpx_linear_kernel<F, NPAD, KS_, NG_>;
     CUtensorMap map;
     if (cudaError_t e = make_act_map(L, NPAD, C::kKS, &map)) return e;
+    CUtensorMap hi_map, lo_map;
+    if (cudaError_t e = make_stream_map(L.s_hi, FmtTraits<F>::kBitsHi, L.rows_p / 64, L.cols_p / 64, C::kKS, &hi_map))
+        return e;
+    if (cudaError_t e = make_stream_map(L.s_lo, FmtTraits<F>::kBitsLo, L.rows_p / 64, L.cols_p / 64, C::kKS, &lo_map))
+        return e;
     // NPAD = 256 (single accumulator buffer): the intermittent wrong results
     // once measured at split 9 were the stage-ring parity aliasing now ruled
     // out by Cfg (kStages >= NG + kAStages).
     KParams kq = kp;
     if (C::kAccBufs == 1) grid = static_cast<int>(kq.units);
     if (cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::kSmemBytes)) return e;
-    kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(map, kq);
+    kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(map, hi_map, lo_map, kq);
     return cudaGetLastError();
 }
 

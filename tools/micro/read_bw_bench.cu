@@ -1,0 +1,147 @@
+// Micro-benchmark (bring-up only): steady-state HBM READ bandwidth on B200,
+// i.e. the ceiling a weight-streaming kernel can approach, measured with a
+// stream long enough (2 GiB per launch) that launch ramp and tail vanish,
+// and the same readers over 135 MB (one llama-65B FP6 weight) for the
+// per-launch overhead.
+//   A  1-D TMA bulk copies into an SMEM ring, 1 consumer warp releasing
+//      slots at once (CTAs/SM x stages x chunk swept)
+//   B  LDG.128 streaming, many warps, 8 independent loads in flight/thread
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_2401_14112_b200/csrc -o read_bw_bench read_bw_bench.cu
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#include "ptx_sm100.cuh"
+
+using namespace fpxk;
+
+struct TArgs {
+    const uint8_t* src;
+    size_t total;
+    int chunk;
+    int stages;
+    unsigned long long* sink;
+};
+
+__global__ void __launch_bounds__(64) tma_read(TArgs a) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t full[32], empty[32];
+    const uint32_t warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < a.stages; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const size_t nchunks = a.total / a.chunk;
+    const size_t c0 = nchunks * blockIdx.x / gridDim.x, c1 = nchunks * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t pol = policy_evict_first();
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t i = 0;
+            for (size_t c = c0; c < c1; ++c, ++i) {
+                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1u;
+                if (i >= (uint32_t)a.stages) mbar_wait(&empty[s], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[s], a.chunk);
+                bulk_g2s(sm + (size_t)s * a.chunk, a.src + c * a.chunk, a.chunk, &full[s], pol);
+            }
+        }
+    } else {
+        uint32_t i = 0, acc = 0;
+        for (size_t c = c0; c < c1; ++c, ++i) {
+            const uint32_t s = i % a.stages, ph = (i / a.stages) & 1u;
+            mbar_wait(&full[s], ph);
+            acc ^= lds32(smem_u32(sm + (size_t)s * a.chunk + 4 * (threadIdx.x & 31)));
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        }
+        if (acc == 0x12345679u) atomicAdd(a.sink, 1ull);
+    }
+}
+
+__global__ void __launch_bounds__(512) ldg_read(const uint4* __restrict__ src, size_t nvec,
+                                                unsigned long long* sink) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    size_t i = tid;
+    for (; i + 7 * stride < nvec; i += 8 * stride) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    for (; i < nvec; i += stride) {
+        const uint4 v = __ldcs(src + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345679u) atomicAdd(sink, 1ull);
+}
+
+#define CK(x)                                                                   \
+    do {                                                                        \
+        cudaError_t e_ = (x);                                                   \
+        if (e_ != cudaSuccess) {                                                \
+            printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+            return 1;                                                           \
+        }                                                                       \
+    } while (0)
+
+int main() {
+    const size_t big = size_t(2) << 30, small = 135266304;
+    const int copies = 3;  // small runs rotate 3 copies (> L2)
+    uint8_t* buf;
+    CK(cudaMalloc(&buf, big + copies * small + 4096));
+    CK(cudaMemset(buf, 1, big + copies * small + 4096));
+    unsigned long long* sink;
+    CK(cudaMalloc(&sink, 8));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    auto time_it = [&](auto&& launch, int reps) {
+        launch(0);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r) launch(r);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        return ms * 1e3 / reps;  // us per launch
+    };
+    struct TC { int cps, stages, chunk; };
+    std::vector<TC> tcs = {{1, 12, 16384}, {1, 6, 32768}, {1, 24, 8192}, {1, 13, 12288}, {1, 4, 49152},
+                           {2, 6, 16384}, {2, 12, 8192}, {3, 4, 16384}, {4, 6, 8192}, {1, 3, 65536}};
+    for (const auto& t : tcs) {
+        const int smem = t.stages * t.chunk;
+        if (cudaFuncSetAttribute(tma_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) continue;
+        const int grid = nsm * t.cps;
+        auto big_l = [&](int) {
+            TArgs a{buf, big, t.chunk, t.stages, sink};
+            tma_read<<<grid, 64, smem>>>(a);
+        };
+        auto small_l = [&](int r) {
+            TArgs a{buf + big + (r % copies) * small, small, t.chunk, t.stages, sink};
+            tma_read<<<grid, 64, smem>>>(a);
+        };
+        const double ub = time_it(big_l, 3), us = time_it(small_l, 12);
+        printf("TMA %d CTA/SM x %2d stages x %6d B (%3d KB in flight/SM): 2 GiB %7.1f us = %6.0f GB/s | 135 MB b2b %5.1f us = %6.0f GB/s\n",
+               t.cps, t.stages, t.chunk, t.cps * smem / 1024, ub, big / ub / 1e3, us, small / us / 1e3);
+        CK(cudaGetLastError());
+    }
+    for (int bps : {2, 4, 8}) {
+        const int grid = nsm * bps;
+        auto big_l = [&](int) { ldg_read<<<grid, 512>>>(reinterpret_cast<const uint4*>(buf), big / 16, sink); };
+        auto small_l = [&](int r) {
+            ldg_read<<<grid, 512>>>(reinterpret_cast<const uint4*>(buf + big + (r % copies) * small), small / 16, sink);
+        };
+        const double ub = time_it(big_l, 3), us = time_it(small_l, 12);
+        printf("LDG %d CTA/SM x 512 thr x 8 x 16 B: 2 GiB %7.1f us = %6.0f GB/s | 135 MB b2b %5.1f us = %6.0f GB/s\n", bps,
+               ub, big / ub / 1e3, us, small / us / 1e3);
+        CK(cudaGetLastError());
+    }
+    printf("done\n");
+    return 0;
+}
