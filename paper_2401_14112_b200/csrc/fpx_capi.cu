@@ -466,9 +466,10 @@ static bool act_needs_stage(const uint16_t* act, uint32_t k_act, uint32_t cols_p
 
 // Workspace layout: [split-K arrival counters, kLinearCounterBytes, always at
 // offset 0 so they stay valid (self-cleaning) across calls of any shape]
-// [fp32 split-K partials][staged activations].
+// [fp32 split-K partials][staged activations][N <= 32: the activations'
+// e4m3 split for the kind::f8f6f4 units (B8, then per-chunk column scales)].
 struct WsLayout {
-    size_t part_off, stage_off, total;
+    size_t part_off, stage_off, split_off, split_bytes, total, total_x8;
 };
 
 static WsLayout ws_layout(uint32_t rows_p, uint32_t cols_p, uint32_t n, int split_k, bool stage) {
@@ -476,7 +477,10 @@ static WsLayout ws_layout(uint32_t rows_p, uint32_t cols_p, uint32_t n, int spli
     WsLayout l;
     l.part_off = kLinearCounterBytes;
     l.stage_off = l.part_off + align256(linear_workspace_bytes(rows_p, nb, split_k));
-    l.total = l.stage_off + (stage ? align256(static_cast<size_t>(cols_p) * n * sizeof(uint16_t)) : 0);
+    l.split_off = l.stage_off + (stage ? align256(static_cast<size_t>(cols_p) * n * sizeof(uint16_t)) : 0);
+    l.split_bytes = linear_x8_enabled() ? linear_split_bytes(cols_p, nb, split_k) : 0;
+    l.total = l.split_off;  // required; the split area is optional (without it N <= 32 runs kind::f16 only)
+    l.total_x8 = l.split_off + l.split_bytes;
     return l;
 }
 
@@ -484,7 +488,7 @@ size_t fpx_linear_workspace_size(uint32_t rows_p, uint32_t cols_p, uint32_t k_ac
     if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
     // A 16-byte-misaligned activation pointer also needs the staging area;
     // callers passing such pointers should size with k_act != cols_p.
-    return ws_layout(rows_p, cols_p, n, split_k, k_act != cols_p).total;
+    return ws_layout(rows_p, cols_p, n, split_k, k_act != cols_p).total_x8;
 }
 
 static int linear_impl(const uint8_t* const* streams, int nseg, const uint16_t* scales, uint32_t rows_p,
@@ -568,6 +572,11 @@ static int linear_impl(const uint8_t* const* streams, int nseg, const uint16_t* 
         L.trace = debug_trace_buffer();
         L.prog = debug_progress_buffer();
         L.pdl_cap = pdl_cap;
+        if (lay.split_bytes != 0 && L.n <= 32 && workspace_bytes >= lay.total_x8) {
+            const uint32_t npad = L.n <= 16 ? 16u : 32u;
+            L.b8 = ws + lay.split_off;
+            L.colf = reinterpret_cast<float*>(ws + lay.split_off + align256(static_cast<size_t>(3) * npad * cols_p));
+        }
         const cudaError_t err = launch_linear(L, s);
         if (err != cudaSuccess) {
             // A launch that did not run to completion may leave split-K
@@ -697,7 +706,7 @@ size_t fpx_linear_sharded_workspace_size(uint32_t rows_p, uint32_t cols_p, uint3
     const uint32_t slot = shard_slot_rows(rows_p, world);
     if (split_k == -1) split_k = fpx_linear_default_split(slot, cols_p, n);
     if (split_k <= 0) split_k = fpx_linear_default_split(rows_p, cols_p, n);
-    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
+    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total_x8);
     return lin + align256(size_t(slot) * n * 4) + align256(size_t(world) * slot * n * 4);
 }
 
@@ -725,7 +734,7 @@ int fpx_linear_sharded(const uint8_t* const* shard_streams, int nseg, const uint
     if (workspace == nullptr || workspace_bytes < need)
         return fail(FPX_ERR_INVALID_VALUE, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
     uint8_t* ws = static_cast<uint8_t*>(workspace);
-    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total);
+    const size_t lin = align256(ws_layout(slot, cols_p, n, split_k, k_act != cols_p).total_x8);
     float* local = reinterpret_cast<float*>(ws + lin);
     float* gathered = reinterpret_cast<float*>(ws + lin + align256(size_t(slot) * n * 4));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

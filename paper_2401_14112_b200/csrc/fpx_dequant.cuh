@@ -122,15 +122,18 @@ FPX_DEV uint32_t shr(uint32_t x) {
 #endif
 }
 
+FPX_DEV uint32_t prmt2(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
 // Codes of iteration j in bits [5:0] of each byte lane (bits 7:6 junk,
-// ignored by the converts), byte lanes already permuted {1,3,0,2} so that
-// the low half feeds R1 (codes 4j+0, 4j+1) and the high half R2 (4j+2,
-// 4j+3).  All stitch operations are byte-local, so the lane permutation is
-// applied once to each of the three packed words (3 PRMT per slice rather
-// than one per iteration).
+// ignored by the converts and by tcgen05.mma kind::f8f6f4), in the byte-lane
+// order of the inputs.  Every operation is byte-local, so permuting the
+// input words' bytes permutes the outputs' bytes the same way.
 template <int F>
-FPX_DEV void codes_low6(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (&c)[4]) {
-    const uint32_t pa = prmt(wa, 0x2031u), pb = prmt(wb, 0x2031u), pc = prmt(wc, 0x2031u);
+FPX_DEV void codes_low6_raw(uint32_t pa, uint32_t pb, uint32_t pc, int h, uint32_t (&c)[4]) {
     if constexpr (FmtTraits<F>::kBitsHi == 2) {
         // 2-bit group j (bits 7-2j..6-2j) -> bits 5:4; 4-bit group j%2 -> bits 3:0
         c[0] = lop3_sel<0x30303030u>(shr<2>(pa), shr<4>(pb));
@@ -149,6 +152,39 @@ FPX_DEV void codes_low6(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (
             c[j] = (hi & 0x3c3c3c3cu) | (lo & 0x02020202u);
         }
     }
+}
+
+// The fp16 path: byte lanes permuted {1,3,0,2} first so that the low half of
+// c[j] feeds R1 (codes 4j+0, 4j+1) and the high half R2 (4j+2, 4j+3); the
+// permutation is applied once to each of the three packed words (3 PRMT per
+// slice rather than one per iteration).
+template <int F>
+FPX_DEV void codes_low6(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (&c)[4]) {
+    codes_low6_raw<F>(prmt(wa, 0x2031u), prmt(wb, 0x2031u), prmt(wc, 0x2031u), h, c);
+}
+
+// ------------------------------------------------------------ 8-bit A path
+// The A operand of tcgen05.mma kind::f8f6f4 straight from the packed words:
+// FP6 codes (FP5 e2m2 as e2m3, see codes_low6_raw) in 8-bit containers, no
+// conversion at all.  In the raw byte-lane order, c[j] holds (lane 1, lane 3)
+// = row 16c + t/4 and (lane 0, lane 2) = row 16c + 8 + t/4, columns
+// 8(j%2) + 2(t%4) + {0, 1} of the slice (c = 2h + j/2; prepack.cpp:17, 29-58).
+// One PRMT per output gathers the four codes of one row:
+//   x[lc][hf] = row 16(2h+lc) + 8hf + t/4, slice columns
+//               {2j, 2j+1, 8+2j, 9+2j} (j = t % 4) in bytes 0..3.
+// 4 LOP3 + 5 shifts + 4 PRMT per 16 weights, vs 3 PRMT + 4 LOP3 + 5 shifts +
+// 8 F2FP on the fp16 path.  The TMEM cell (row, column 4s + t%4) of a k-tile
+// then holds logical k = 16s + 4(t%4) + b <- actual slice column
+// {2j, 2j+1, 8+2j, 9+2j}[b]; the activations' e4m3 parts are laid out in
+// the same logical K order (act_split_kernel), so the products pair up.
+template <int F>
+FPX_DEV void codes8_slice_half(uint32_t wa, uint32_t wb, uint32_t wc, int h, uint32_t (&x)[2][2]) {
+    uint32_t c[4];
+    codes_low6_raw<F>(wa, wb, wc, h, c);
+    x[0][0] = prmt2(c[0], c[1], 0x7531u);
+    x[0][1] = prmt2(c[0], c[1], 0x6420u);
+    x[1][0] = prmt2(c[2], c[3], 0x7531u);
+    x[1][1] = prmt2(c[2], c[3], 0x6420u);
 }
 
 // ------------------------------------------------------------ kSwar path

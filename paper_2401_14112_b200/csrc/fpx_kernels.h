@@ -60,8 +60,15 @@ struct LinearLaunch {
     // weights / scales on the same stream, so nothing is read before
     // griddepcontrol.wait; 2 = no cap.
     uint32_t pdl_cap = 2;
+    // N <= 32: workspace for the activations' e4m3 split (kind::f8f6f4 units of
+    // the decode kernel): b8 [3 * npad(n)][cols_p] bytes, colf [split][npad(n)]
+    // floats; null = kind::f16 only.
+    uint8_t* b8 = nullptr;
+    float* colf = nullptr;
 };
 
 cudaError_t launch_linear(const LinearLaunch& p, cudaStream_t st);
 size_t linear_workspace_bytes(uint32_t rows_p, uint32_t n, int split);
+size_t linear_split_bytes(uint32_t cols_p, uint32_t n, int split);  // b8 + colf (0 when n > 32)
+bool linear_x8_enabled();  // FPX_LINEAR_X8=1: the opt-in kind::f8f6f4 kernel for N <= 32
 int linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n, int num_sms);

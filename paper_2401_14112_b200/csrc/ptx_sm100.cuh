@@ -255,6 +255,20 @@ FPX_DEV void umma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
         : "memory");
 }
 
+// kind::f8f6f4 (A = FP6/FP8 codes in 8-bit containers from TMEM, B = FP8
+// from shared memory, K = 32 per instruction), warp-wide with one elected
+// issuer like umma_f16_ts_warp.
+FPX_DEV void umma_f8f6f4_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 FPX_DEV void umma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -283,6 +297,14 @@ FPX_DEV void tmem_st_16x128b_x8(uint32_t taddr, const uint32_t (&r)[16]) {
         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
         "r"(r[15])
         : "memory");
+}
+
+// 16 lanes x 16 columns: 16x128b repeated 4 times (register 2i -> lane base
+// + t/4, col 4i + t%4; register 2i+1 -> lane base + 8 + t/4).
+FPX_DEV void tmem_st_16x128b_x4(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 
 FPX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -320,6 +342,12 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t m, uint32_t n) {
            | (0u << 10)         // B f16
            | ((n >> 3) << 17)   // N / 8
            | ((m >> 4) << 24);  // M / 16
+}
+
+// Instruction descriptor, kind::f8f6f4: D=f32, A/B formats (MXF8F6F4:
+// e4m3 0, e5m2 1, e2m3 3, e3m2 4, e2m1 5), both K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_f8f6f4(uint32_t m, uint32_t n, uint32_t a_fmt, uint32_t b_fmt) {
+    return (1u << 4) | (a_fmt << 7) | (b_fmt << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
 // ---------------------------------------------------------------- fp16

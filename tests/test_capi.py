@@ -29,7 +29,8 @@ def test_library_is_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
-    for mnemonic in ("UTCHMMA", "UTMALDG", "UBLKCP", "STTM", "LDTM", "F2FP.F16.E3M2.UNPACK_B"):
+    # UTCHMMA: tcgen05.mma kind::f16; UTCQMMA: kind::f8f6f4 (fpx_linear_x8.cu)
+    for mnemonic in ("UTCHMMA", "UTCQMMA", "UTMALDG", "STTM", "LDTM", "F2FP.F16.E3M2.UNPACK_B"):
         assert mnemonic in sass, mnemonic
 
 

@@ -746,3 +746,23 @@ def test_compute_sanitizer(cuda, tool):
     print(out[-2000:])
     assert r.returncode == 0 and "sanitize driver ok" in out, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
+
+
+def test_x8_kernel_parity_subprocess(cuda):
+    """The opt-in kind::f8f6f4 kernel (FPX_LINEAR_X8=1, fpx_linear_x8.cu: FP6
+    codes x the activations' exact three-part e4m3 split) through the same
+    parity tests as the default path: golden C, oracle C for 3 formats x
+    shapes x N <= 300, edge values (kind::f16 fallback units for tiny /
+    huge scales in the same launch), the scale-placement boundaries,
+    split-K determinism and grid independence, bit-identical shards and the
+    PDL back-to-back stress.  A separate process: the switch is read once."""
+    if os.environ.get("FPX_LINEAR_X8"):
+        pytest.skip("already inside the X8 run")
+    sel = ("linear_vs_golden or linear_batches_and_shapes or linear_edge_values or scale_placement or "
+           "split_k_deterministic or sharded_rows_bit_identical or pdl_back_to_back or linear_fused_epilogue")
+    env = dict(os.environ, FPX_LINEAR_X8="1")
+    r = subprocess.run(["python", "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-q", "-x", "-m", "gpu",
+                        "-k", sel, "-p", "no:cacheprovider"], capture_output=True, text=True, timeout=900, env=env,
+                       cwd=ROOT)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]

@@ -13,6 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
+last_mhz = 0
+
 import paper_2401_14112_b200 as fpx  # noqa: E402
 
 dev = torch.device("cuda:0")
@@ -36,7 +38,39 @@ def run(n, split, act, out, i):
     assert st == 0, L.fpx_last_error()
 
 
-def timeit(n, split, iters=30):
+class Clocks:
+    """SM clock samples (NVML, ~1 ms) while a timing runs: power-capped
+    clocks move the compute-bound variants."""
+
+    def __init__(self):
+        import threading
+        import pynvml
+        pynvml.nvmlInit()
+        self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(0)
+        self.samples, self.on, self.threading = [], False, threading
+
+    def __enter__(self):
+        self.samples, self.on = [], True
+
+        def loop():
+            while self.on:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+        self.t = self.threading.Thread(target=loop, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.on = False
+        self.t.join()
+
+    def median(self):
+        return sorted(self.samples)[len(self.samples) // 2] if self.samples else 0
+
+
+CLK = Clocks() if os.environ.get("CLOCKS") else None
+
+
+def timeit(n, split, iters=int(os.environ.get("ITERS", 30))):
     """Device time per launch: `iters` launches captured in one CUDA graph and
     replayed (host launch overhead excluded; the plain launch loop is
     host-bound at ~20 us per call through ctypes)."""
@@ -52,10 +86,21 @@ def timeit(n, split, iters=30):
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    g.replay()
-    e1.record()
-    torch.cuda.synchronize()
+    global last_mhz
+    if CLK:
+        with CLK:
+            for _ in range(20):  # ~20 x iters launches: long enough to sample the clock under load
+                g.replay()
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+        last_mhz = CLK.median()
+    else:
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
     err = None
     if not os.environ.get("FPX_LINEAR_DBG"):
         run(n, split, act, out, 0)
@@ -85,5 +130,6 @@ for kern in ["decode"]:
                     print(f"  .. {kern} cfg={cfg} n={n} split={sp} dbg{v}", flush=True)
                     us, err = timeit(n, sp)
                     os.environ.pop("FPX_LINEAR_DBG", None)
-                    row.append(f"dbg{v}={us:6.1f}us({wbytes / us / 1e3:5.0f}GB/s)" + (f" err={err:.1e}" if err is not None else ""))
+                    row.append(f"dbg{v}={us:6.1f}us({wbytes / us / 1e3:5.0f}GB/s)" + (f" err={err:.1e}" if err is not None else "")
+                               + (f" {last_mhz}MHz" if CLK else ""))
                 print(f"{kern:8s} cfg={cfg} n={n:3d} split={sp:2d} " + " ".join(row), flush=True)

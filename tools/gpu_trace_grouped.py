@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 import paper_2401_14112_b200 as fpx  # noqa: E402
 
-exec(open(os.path.join(ROOT, "tests", "gpu_prof_one.py")).read().split("for _ in range(int(os.environ")[0])
+exec(open(os.path.join(ROOT, "tools", "gpu_prof_one.py")).read().split("for _ in range(int(os.environ")[0])
 for _ in range(3):
     st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, fmt.exp_bits, fmt.man_bits, act.data_ptr(), K, n,
                       out.data_ptr(), M, split, ws.data_ptr(), ws.numel(), s)

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("FPX_B200_LIB", os.path.join(ROOT, "paper_2401_14112_b200", "libfpx_b200_trace.so"))  # make ... trace
 import torch  # noqa: E402
 
-exec(open(os.path.join(ROOT, "tests", "gpu_prof_one.py")).read().split("for _ in range(int(os.environ")[0])
+exec(open(os.path.join(ROOT, "tools", "gpu_prof_one.py")).read().split("for _ in range(int(os.environ")[0])
 for _ in range(4):  # calls 0..3 -> buffers 0,1,0,1: the last two launches are consecutive
     st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, fmt.exp_bits, fmt.man_bits, act.data_ptr(), K, n,
                       out.data_ptr(), M, split, ws.data_ptr(), ws.numel(), s)

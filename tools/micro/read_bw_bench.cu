@@ -131,6 +131,21 @@ int main() {
                t.cps, t.stages, t.chunk, t.cps * smem / 1024, ub, big / ub / 1e3, us, small / us / 1e3);
         CK(cudaGetLastError());
     }
+    // per-SM TMA ceiling: fewer CTAs than SMs (1 CTA/SM placement), same 192 KB ring
+    for (int grid : {32, 64, 96, 128, 148}) {
+        for (int chunk : {12288, 16384, 49152}) {
+            const int stages = (chunk == 12288 ? 16 : 196608 / chunk);
+            const int smem = stages * chunk;
+            cudaFuncSetAttribute(tma_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            auto big_l = [&](int) {
+                TArgs a{buf, big / 4, chunk, stages, sink};
+                tma_read<<<grid, 64, smem>>>(a);
+            };
+            const double ub = time_it(big_l, 3);
+            printf("TMA grid %3d x %2d stages x %6d B: 512 MiB %7.1f us = %6.0f GB/s = %5.1f GB/s per CTA\n", grid, stages,
+                   chunk, ub, big / 4 / ub / 1e3, big / 4 / ub / 1e3 / grid);
+        }
+    }
     for (int bps : {2, 4, 8}) {
         const int grid = nsm * bps;
         auto big_l = [&](int) { ldg_read<<<grid, 512>>>(reinterpret_cast<const uint4*>(buf), big / 16, sink); };
