@@ -8,6 +8,7 @@
 // staging for unaligned K, and the sharded-output gather permute).
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "fpx_dequant.cuh"
@@ -21,22 +22,44 @@ namespace fpxk {
 // scale check (:155-164), then codes = RNE-encode(double(v) / s) (:168-170).
 // Failures are folded into one 64-bit atomicMin key (row << 8 | status) so
 // the host sees the FIRST failing row in row order (:173-174).
+//
+// The encode runs without any division (encode_exact).  The reference rounds
+// q = double(w) / s to nearest in double, then rounds q to the format:
+// ex = floor(log2 q) (>= emin), k = rint(q * 2^(m - ex)) ties-to-even,
+// saturating at max_rep.  Here q is formed in fp32 as |w| * fp32(1/s), whose
+// relative error (<= 2^-23) moves y = q * 2^(m - ex) < 2^(m+1) by at most
+// 2^(m-22); so rint(y) is the reference's k unless y lies within
+// eps = 2^(m-20) of a half-integer, and those rare cases are decided
+// exactly: the midpoint T = (floor(y) + 1/2) * 2^(ex - m) * s has at most
+// m + 2 + 11 significant bits, so it is exact in fp32, and |w| compares
+// exactly against it (the double quotient of the reference cannot make a
+// tie out of |w| != T: both sit on |w|'s ulp grid, >= 2^-24 |w| apart).  An
+// exact tie goes to the even k, like the reference's rint.  A quotient that
+// rounds across a power of two only moves k to the next binade's first
+// code, which is the same code.  Values above the largest code round to it
+// (min with cmax), which is the reference's saturation.
 
-__device__ __forceinline__ uint32_t encode_dev(double v, int e, int m, int bias, double maxrep) {
-    const uint32_t smask = 1u << (e + m);
-    const uint32_t sign = signbit(v) ? smask : 0u;
-    const double a = fabs(v);
-    if (a > maxrep) return sign | (smask - 1u);
-    const int emin = 1 - bias;
-    int ex = (a >= ldexp(1.0, emin)) ? ilogb(a) : emin;
-    uint32_t k = static_cast<uint32_t>(rint(ldexp(a, m - ex)));  // ties-to-even
-    const uint32_t unit = 1u << m;
-    if (k == 2u * unit) {
-        k = unit;
-        ++ex;
+// The reference's encode(double(w) / s) for s > 0 (sv = s, inv = fp32 1/s).
+__device__ __forceinline__ uint32_t encode_exact(float w, float sv, float inv, int e, int m, int bias,
+                                                 uint32_t cmax) {
+    const uint32_t sign = (__float_as_uint(w) >> 31) << (e + m);
+    const float a = fabsf(w);
+    const float q = a * inv;
+    int ex = static_cast<int>((__float_as_uint(q) >> 23) & 0xffu) - 127;
+    ex = min(max(ex, 1 - bias), 120);
+    const float y = q * __uint_as_float(static_cast<uint32_t>(127 + m - ex) << 23);  // q * 2^(m - ex), exact
+    float kf = rintf(y);
+    const float eps = __uint_as_float(static_cast<uint32_t>(127 + m - 20) << 23);
+    if (fabsf(y - kf) > 0.5f - eps) {
+        // near a tie: compare against the exact midpoint
+        const float fl = floorf(y);
+        const float t = (fl + 0.5f) * __uint_as_float(static_cast<uint32_t>(127 + ex - m) << 23) * sv;
+        kf = a > t ? fl + 1.0f : (a < t ? fl : fl + (fmodf(fl, 2.0f) != 0.0f ? 1.0f : 0.0f));
     }
-    if (k < unit) return sign | k;
-    return sign | (static_cast<uint32_t>(ex + bias) << m) | (k - unit);
+    const uint32_t k = static_cast<uint32_t>(kf);
+    const uint32_t unit = 1u << m;
+    uint32_t c = k < unit ? k : (static_cast<uint32_t>(ex + bias) << m) + k - unit;
+    return sign | min(c, cmax);
 }
 
 template <typename T>
@@ -50,6 +73,29 @@ __device__ __forceinline__ float load_w<uint16_t>(const uint16_t* p) {
     return __half2float(__ushort_as_half(*p));  // exact (codec.cpp:35-40)
 }
 
+// Four consecutive weights of a row (vector load when aligned).
+template <typename T>
+__device__ __forceinline__ float4 load_w4(const T* p, bool vec);
+template <>
+__device__ __forceinline__ float4 load_w4<float>(const float* p, bool vec) {
+    if (vec) return __ldcs(reinterpret_cast<const float4*>(p));
+    return make_float4(p[0], p[1], p[2], p[3]);
+}
+template <>
+__device__ __forceinline__ float4 load_w4<uint16_t>(const uint16_t* p, bool vec) {
+    uint32_t lo, hi;
+    if (vec) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(p));
+        lo = v.x, hi = v.y;
+    } else {
+        lo = p[0] | (static_cast<uint32_t>(p[1]) << 16), hi = p[2] | (static_cast<uint32_t>(p[3]) << 16);
+    }
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&lo));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// Row pass: scale + status (+ the row's codes when codes != nullptr).
 // codes == nullptr: row scales, status and the per-row skip flag only (pass 1
 // of the fused quantize+pack, whose tile kernel encodes and packs).
 template <typename T>
@@ -67,22 +113,45 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
     }
     __shared__ float red[8];
     __shared__ int nan_flag;
-    __shared__ double s_val;
+    __shared__ float s_val;
     __shared__ int skip;
     if (r >= rows) {  // padding rows: codes 0, scale 1.0
-        for (uint32_t c = threadIdx.x; c < cols_p; c += blockDim.x) out[c] = 0;
+        for (uint32_t c = threadIdx.x * 16; c < cols_p; c += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(out + c) = make_uint4(0u, 0u, 0u, 0u);
         if (threadIdx.x == 0) scales[r] = 0x3c00u;
         return;
     }
     const T* row = w + static_cast<size_t>(r) * cols;
+    // vector loads when the row start is 16-byte (fp32) / 8-byte (fp16) aligned
+    const bool vec = (reinterpret_cast<uintptr_t>(row) % (4 * sizeof(T))) == 0;
+    const uint32_t c4 = cols & ~3u;
     if (threadIdx.x == 0) nan_flag = 0;
     __syncthreads();
     float amax = 0.0f;
     bool nan = false;
-    for (uint32_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    // eight independent vector loads in flight per thread (the row is
+    // streamed once here and once more, mostly from L2, by the encode)
+    constexpr uint32_t kU = 8;
+    uint32_t c = threadIdx.x * 4;
+    for (; c + (kU - 1) * blockDim.x * 4 < c4; c += kU * blockDim.x * 4) {
+        float4 v[kU];
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) v[u] = load_w4(row + c + u * blockDim.x * 4, vec);
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            nan |= isnan(v[u].x) | isnan(v[u].y) | isnan(v[u].z) | isnan(v[u].w);
+            amax = fmaxf(fmaxf(amax, fmaxf(fabsf(v[u].x), fabsf(v[u].y))), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+        }
+    }
+    for (; c < c4; c += blockDim.x * 4) {
+        const float4 v = load_w4(row + c, vec);
+        nan |= isnan(v.x) | isnan(v.y) | isnan(v.z) | isnan(v.w);
+        amax = fmaxf(fmaxf(amax, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));  // fmaxf drops NaN
+    }
+    for (uint32_t c = c4 + threadIdx.x; c < cols; c += blockDim.x) {
         const float a = fabsf(load_w(row + c));
         nan |= isnan(a);
-        amax = fmaxf(amax, a);  // fmaxf drops NaN; tracked separately
+        amax = fmaxf(amax, a);
     }
     if (nan) nan_flag = 1;
 #pragma unroll
@@ -119,27 +188,68 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
         }
         scales[r] = s16;
         if (row_skip) row_skip[r] = static_cast<uint8_t>(skip);
-        s_val = static_cast<double>(__half2float(__ushort_as_half(s16)));
+        s_val = __half2float(__ushort_as_half(s16));
     }
     if (codes == nullptr) return;
     __syncthreads();
     const int bias = (1 << (e - 1)) - 1;
-    const double sv = s_val;
+    const float sv = s_val, inv = __frcp_rn(s_val);
+    const uint32_t cmax = (1u << (e + m)) - 1u;
     const bool zero = skip != 0;
-    for (uint32_t c = threadIdx.x; c < cols_p; c += blockDim.x) {
-        uint8_t code = 0;
-        if (!zero && c < cols) code = static_cast<uint8_t>(encode_dev(static_cast<double>(load_w(row + c)) / sv, e, m, bias, maxrep));
-        out[c] = code;
+    // 4 codes (one 32-bit store) per thread and vector; four vectors in
+    // flight per iteration over the row's full-width part, then the tail
+    constexpr uint32_t kE = 4;
+    const uint32_t step = blockDim.x * 4;
+    uint32_t c0 = threadIdx.x * 4;
+    if (!zero) {
+        for (; c0 + (kE - 1) * step + 4 <= cols; c0 += kE * step) {
+            float4 v[kE];
+#pragma unroll
+            for (uint32_t u = 0; u < kE; ++u) v[u] = load_w4(row + c0 + u * step, vec);
+#pragma unroll
+            for (uint32_t u = 0; u < kE; ++u) {
+                const uint32_t packed = encode_exact(v[u].x, sv, inv, e, m, bias, cmax) |
+                                        encode_exact(v[u].y, sv, inv, e, m, bias, cmax) << 8 |
+                                        encode_exact(v[u].z, sv, inv, e, m, bias, cmax) << 16 |
+                                        encode_exact(v[u].w, sv, inv, e, m, bias, cmax) << 24;
+                *reinterpret_cast<uint32_t*>(out + c0 + u * step) = packed;
+            }
+        }
+    }
+    for (uint32_t c = c0; c < cols_p; c += step) {
+        uint32_t packed = 0;
+        if (!zero && c < cols) {
+            float4 v;
+            if (c + 4 <= cols) {
+                v = load_w4(row + c, vec);
+            } else {
+                v.x = load_w(row + c);
+                v.y = c + 1 < cols ? load_w(row + c + 1) : 0.0f;
+                v.z = c + 2 < cols ? load_w(row + c + 2) : 0.0f;
+                v.w = c + 3 < cols ? load_w(row + c + 3) : 0.0f;
+            }
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c + j < cols) packed |= encode_exact(vv[j], sv, inv, e, m, bias, cmax) << (8 * j);
+        }
+        *reinterpret_cast<uint32_t*>(out + c) = packed;
     }
 }
 
 // ------------------------------------------------------------------ K1
 // One warp per 64x64 tile.  The tile's codes are staged in shared memory
-// with coalesced 16-byte row loads; thread t then walks its 128 codes in
-// consumption order (slice, chunk, pair, lane -> prepack.cpp:29-58) and
-// ORs each segment into its word (prepack.cpp:71-86); word j is stored at
-// (j*32+t)*4 of the tile block -- every store instruction is one coalesced
-// 128-byte row (prepack.cpp:115-134).
+// (coalesced 16-byte row loads; row stride 80 bytes so the eight rows one
+// gather instruction touches fall on eight different bank groups).  Thread t
+// then builds its words iteration by iteration: iteration it = (slice s,
+// chunk c, column half ph) holds the four codes (rows r0, r0 + 8) x (columns
+// c0, c0 + 1), r0 = 16c + t/4, c0 = 16s + 8ph + 2(t%4) (prepack.cpp:29-58),
+// fetched with two 16-bit shared loads and placed into byte lanes {1, 3, 0,
+// 2} (prepack.cpp:17) with one PRMT.  Each segment of width w is then cut out
+// of all four lanes at once (SWAR: shift, mask) and shifted to bits
+// 8 - w(g+1) of its lane (prepack.cpp:71-86); word j is stored at
+// (j*32+t)*4 of the tile block, one coalesced 128-byte row per store
+// instruction (prepack.cpp:115-134).
 struct SplitDesc {
     int nseg;
     int width[3];
@@ -152,6 +262,7 @@ struct SplitDescC {
 };
 
 constexpr int kPackWarps = 4;
+constexpr int kTileStride = 80;  // bytes per staged 64-code row
 
 __device__ __forceinline__ void code_rc(uint32_t t, uint32_t k, uint32_t& r, uint32_t& c) {
     const uint32_t s = k >> 5, ch = (k >> 3) & 3u, p = (k >> 1) & 3u, l = k & 1u;
@@ -161,55 +272,92 @@ __device__ __forceinline__ void code_rc(uint32_t t, uint32_t k, uint32_t& r, uin
 
 __constant__ uint32_t kLane[4] = {1u, 3u, 0u, 2u};
 
-__global__ void __launch_bounds__(32 * kPackWarps) prepack_kernel(const uint8_t* __restrict__ codes,
-                                                                  uint32_t cols_p, uint32_t ntiles,
-                                                                  int bits, SplitDesc sd) {
-    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * 64];
-    const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
-    const uint32_t tile = blockIdx.x * kPackWarps + warp;
-    if (tile >= ntiles) return;
-    const uint32_t gc = cols_p / 64u;
-    const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
-    uint8_t* ts = tile_s[warp];
+// The four codes of iteration `it` of thread t in byte lanes {1, 3, 0, 2}:
+// lane 1 (r0, c0), lane 3 (r0, c0+1), lane 0 (r0+8, c0), lane 2 (r0+8, c0+1).
+__device__ __forceinline__ uint32_t iter_codes(const uint8_t* ts, uint32_t t, uint32_t it) {
+    const uint32_t s = it >> 3, ch = (it >> 1) & 3u, ph = it & 1u;
+    const uint32_t r0 = 16u * ch + t / 4u, c0 = 16u * s + 8u * ph + 2u * (t % 4u);
+    const uint32_t a = *reinterpret_cast<const uint16_t*>(ts + r0 * kTileStride + c0);
+    const uint32_t b = *reinterpret_cast<const uint16_t*>(ts + (r0 + 8u) * kTileStride + c0);
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, 0x1504;" : "=r"(d) : "r"(a), "r"(b));  // bytes {b.lo, a.lo, b.hi, a.hi}
+    return d;
+}
+
+// Pack a staged tile (stride kTileStride) into its stream blocks: segment
+// of width W at bit `low`, words built in registers from all 32 iterations.
+template <int W>
+__device__ __forceinline__ void pack_segment(const uint32_t (&x)[32], int low, uint8_t* stream, uint32_t t,
+                                             uint32_t tile) {
+    constexpr uint32_t kPer = 8u / W, kWords = 4u * W;
+    constexpr uint32_t kMask = ((1u << W) - 1u) * 0x01010101u;
+    uint32_t* blk = reinterpret_cast<uint32_t*>(stream + static_cast<size_t>(tile) * 512u * W);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t chunk = i * 32u + t;  // 256 x 16-byte chunks
-        const uint32_t rr = chunk >> 2, cc = (chunk & 3u) * 16u;
-        *reinterpret_cast<uint4*>(ts + rr * 64u + cc) =
-            *reinterpret_cast<const uint4*>(codes + static_cast<size_t>(r0 + rr) * cols_p + c0 + cc);
+    for (uint32_t j = 0; j < kWords; ++j) {
+        uint32_t word = 0;
+#pragma unroll
+        for (uint32_t g = 0; g < kPer; ++g) word |= ((x[j * kPer + g] >> low) & kMask) << (8u - W * (g + 1u));
+        blk[j * 32u + t] = word;
     }
-    __syncwarp();
+}
+
+__device__ __forceinline__ void pack_tile(const uint8_t* ts, uint32_t t, uint32_t tile, int bits, const SplitDesc& sd) {
+    uint32_t x[32];
+#pragma unroll
+    for (uint32_t it = 0; it < 32u; ++it) x[it] = iter_codes(ts, t, it);
     int low = bits;
     for (int sg = 0; sg < sd.nseg; ++sg) {
         const int w = sd.width[sg];
         low -= w;
-        const uint32_t per_word = 8u / w, nwords = 4u * w;
-        const uint32_t vmask = (1u << w) - 1u;
-        uint8_t* blk = sd.stream[sg] + static_cast<size_t>(tile) * 512u * w;
-        for (uint32_t j = 0; j < nwords; ++j) {
-            uint32_t word = 0;
-            // codes whose segment lands in word j: iterations j*per_word .. +per_word-1
-            for (uint32_t g = 0; g < per_word; ++g) {
-                const uint32_t it = j * per_word + g;
-#pragma unroll
-                for (uint32_t q = 0; q < 4u; ++q) {
-                    uint32_t rr, cc;
-                    code_rc(t, it * 4u + q, rr, cc);
-                    const uint32_t v = (static_cast<uint32_t>(ts[rr * 64u + cc]) >> low) & vmask;
-                    word |= v << (8u * kLane[q] + 8u - w * (g + 1u));
-                }
-            }
-            reinterpret_cast<uint32_t*>(blk)[j * 32u + t] = word;
+        switch (w) {
+            case 1: pack_segment<1>(x, low, sd.stream[sg], t, tile); break;
+            case 2: pack_segment<2>(x, low, sd.stream[sg], t, tile); break;
+            case 4: pack_segment<4>(x, low, sd.stream[sg], t, tile); break;
+            default: break;  // the C-ABI admits widths 1, 2 and 4 only
         }
+    }
+}
+
+// Persistent warps: each walks tiles gw, gw + nw, ... with the next tile's
+// 4 KB of codes already in flight (registers) while it packs the current one.
+__global__ void __launch_bounds__(32 * kPackWarps) prepack_kernel(const uint8_t* __restrict__ codes,
+                                                                  uint32_t cols_p, uint32_t ntiles,
+                                                                  int bits, SplitDesc sd) {
+    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * kTileStride];
+    const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
+    const uint32_t nw = gridDim.x * kPackWarps;
+    const uint32_t gc = cols_p / 64u;
+    uint8_t* ts = tile_s[warp];
+    auto load = [&](uint32_t tile, uint4 (&v)[8]) {
+        const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t chunk = i * 32u + t;  // 256 x 16-byte chunks
+            v[i] = __ldcs(reinterpret_cast<const uint4*>(codes + static_cast<size_t>(r0 + (chunk >> 2)) * cols_p + c0 +
+                                                         (chunk & 3u) * 16u));
+        }
+    };
+    uint32_t tile = blockIdx.x * kPackWarps + warp;
+    uint4 cur[8];
+    if (tile < ntiles) load(tile, cur);
+    for (; tile < ntiles; tile += nw) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t chunk = i * 32u + t;
+            *reinterpret_cast<uint4*>(ts + (chunk >> 2) * kTileStride + (chunk & 3u) * 16u) = cur[i];
+        }
+        if (tile + nw < ntiles) load(tile + nw, cur);  // next tile in flight
+        __syncwarp();
+        pack_tile(ts, t, tile, bits, sd);
+        __syncwarp();  // ts is rewritten next iteration
     }
 }
 
 // ------------------------------------------------------------------ K0+K1 fused
 // Pass 2 of fpx_quantize_pack: one warp per 64x64 tile encodes its codes
-// straight from the weights (the same fp64 RNE encode of double(w) / s as
-// quantize_kernel, codec.cpp:168-170, with the row scales and skip flags of
-// pass 1) into shared memory, then packs them exactly like prepack_kernel.
-// The code matrix never exists in HBM.
+// straight from the weights (encode_exact with the row scales and skip flags
+// of pass 1) into shared memory, then packs them exactly like
+// prepack_kernel.  The code matrix never touches HBM.
 template <typename T>
 __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T* __restrict__ w, uint32_t rows,
                                                                         uint32_t cols, uint32_t cols_p,
@@ -218,7 +366,7 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
                                                                         const uint16_t* __restrict__ scales,
                                                                         const uint8_t* __restrict__ row_skip,
                                                                         int bits, SplitDesc sd) {
-    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * 64];
+    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * kTileStride];
     const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
     const uint32_t tile = blockIdx.x * kPackWarps + warp;
     if (tile >= ntiles) return;
@@ -226,73 +374,108 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
     const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
     uint8_t* ts = tile_s[warp];
     const int bias = (1 << (e - 1)) - 1;
-    // two rows per pass: lanes 0-15 row 2i, 16-31 row 2i+1, 4 consecutive columns each
-    for (uint32_t i = 0; i < 32u; ++i) {
-        const uint32_t rr = 2u * i + (t >> 4), cc = (t & 15u) * 4u;
-        const uint32_t r = r0 + rr;
-        uint32_t packed4 = 0;
-        if (r < rows && !row_skip[r]) {
-            const double sv = static_cast<double>(__half2float(__ushort_as_half(scales[r])));
-            const T* row = w + static_cast<size_t>(r) * cols;
+    const uint32_t cmax = (1u << (e + m)) - 1u;
+    (void)maxrep;
+    // two rows per pass: lanes 0-15 row 2i, 16-31 row 2i+1, the same 4
+    // consecutive columns every pass.  Passes in chunks of 8 with every load
+    // of the chunk issued first (the loads depend only on indices; row scales
+    // and skip flags load alongside and apply after).
+    const uint32_t cc = (t & 15u) * 4u, c = c0 + cc;
+    const bool full = c + 4u <= cols;
+    const bool vec = (reinterpret_cast<uintptr_t>(w) % 16u) == 0 && (static_cast<size_t>(cols) * sizeof(T)) % 16u == 0;
+    constexpr uint32_t kChunk = 8;
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < 32u; i0 += kChunk) {
+        float4 v[kChunk];
+        uint16_t sraw[kChunk];
+        uint8_t skip[kChunk];
 #pragma unroll
-            for (uint32_t q = 0; q < 4u; ++q) {
-                const uint32_t c = c0 + cc + q;
-                if (c < cols)
-                    packed4 |= encode_dev(static_cast<double>(load_w(row + c)) / sv, e, m, bias, maxrep) << (8u * q);
-            }
-        }
-        *reinterpret_cast<uint32_t*>(ts + rr * 64u + cc) = packed4;
-    }
-    __syncwarp();
-    int low = bits;
-    for (int sg = 0; sg < sd.nseg; ++sg) {
-        const int wd = sd.width[sg];
-        low -= wd;
-        const uint32_t per_word = 8u / wd, nwords = 4u * wd;
-        const uint32_t vmask = (1u << wd) - 1u;
-        uint8_t* blk = sd.stream[sg] + static_cast<size_t>(tile) * 512u * wd;
-        for (uint32_t j = 0; j < nwords; ++j) {
-            uint32_t word = 0;
-            for (uint32_t g = 0; g < per_word; ++g) {
-                const uint32_t it = j * per_word + g;
-#pragma unroll
-                for (uint32_t q = 0; q < 4u; ++q) {
-                    uint32_t rr, cc;
-                    code_rc(t, it * 4u + q, rr, cc);
-                    const uint32_t v = (static_cast<uint32_t>(ts[rr * 64u + cc]) >> low) & vmask;
-                    word |= v << (8u * kLane[q] + 8u - wd * (g + 1u));
+        for (uint32_t j = 0; j < kChunk; ++j) {
+            const uint32_t r = r0 + 2u * (i0 + j) + (t >> 4);
+            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            sraw[j] = 0x3c00u;
+            skip[j] = 1;
+            if (r < rows) {
+                const T* row = w + static_cast<size_t>(r) * cols;
+                sraw[j] = scales[r];
+                skip[j] = row_skip[r];
+                if (full) {
+                    v[j] = load_w4(row + c, vec);
+                } else if (c < cols) {
+                    v[j].x = load_w(row + c);
+                    if (c + 1 < cols) v[j].y = load_w(row + c + 1);
+                    if (c + 2 < cols) v[j].z = load_w(row + c + 2);
                 }
             }
-            reinterpret_cast<uint32_t*>(blk)[j * 32u + t] = word;
         }
+#pragma unroll
+        for (uint32_t j = 0; j < kChunk; ++j) {
+            const uint32_t rr = 2u * (i0 + j) + (t >> 4);
+            uint32_t packed4 = 0;
+            if (!skip[j]) {
+                const float sv = __half2float(__ushort_as_half(sraw[j])), inv = __frcp_rn(sv);
+                const float vv[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+                for (uint32_t q = 0; q < 4u; ++q)
+                    if (c + q < cols) packed4 |= encode_exact(vv[q], sv, inv, e, m, bias, cmax) << (8u * q);
+            }
+            *reinterpret_cast<uint32_t*>(ts + rr * kTileStride + cc) = packed4;
+        }
+    }
+    __syncwarp();
+    pack_tile(ts, t, tile, bits, sd);
+}
+
+// Exact inverse (prepack.cpp:211-260): every segment's words are cut back
+// into the 32 iterations' byte lanes (SWAR), then each iteration's four
+// codes go to their two rows with two 16-bit shared stores and the staged
+// tile leaves as coalesced 16-byte rows.
+template <int W>
+__device__ __forceinline__ void unpack_segment(uint32_t (&x)[32], int low, const uint8_t* stream, uint32_t t,
+                                               uint32_t tile) {
+    constexpr uint32_t kPer = 8u / W, kWords = 4u * W;
+    constexpr uint32_t kMask = ((1u << W) - 1u) * 0x01010101u;
+    const uint32_t* blk = reinterpret_cast<const uint32_t*>(stream + static_cast<size_t>(tile) * 512u * W);
+#pragma unroll
+    for (uint32_t j = 0; j < kWords; ++j) {
+        const uint32_t word = __ldcs(blk + j * 32u + t);
+#pragma unroll
+        for (uint32_t g = 0; g < kPer; ++g) x[j * kPer + g] |= ((word >> (8u - W * (g + 1u))) & kMask) << low;
     }
 }
 
-// Exact inverse: words -> codes -> tile positions.
 __global__ void __launch_bounds__(32 * kPackWarps) unpack_kernel(uint8_t* __restrict__ codes, uint32_t cols_p,
                                                                  uint32_t ntiles, int bits, SplitDescC sd) {
-    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * 64];
+    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * kTileStride];
     const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
     const uint32_t tile = blockIdx.x * kPackWarps + warp;
     if (tile >= ntiles) return;
     const uint32_t gc = cols_p / 64u;
     const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
     uint8_t* ts = tile_s[warp];
-    for (uint32_t k = 0; k < 128u; ++k) {
-        const uint32_t it = k >> 2;
-        uint32_t code = 0;
-        int low = bits;
-        for (int sg = 0; sg < sd.nseg; ++sg) {
-            const int w = sd.width[sg];
-            low -= w;
-            const uint32_t per_word = 8u / w;
-            const uint32_t word = reinterpret_cast<const uint32_t*>(sd.stream[sg] + static_cast<size_t>(tile) * 512u * w)[(it / per_word) * 32u + t];
-            const uint32_t sh = 8u * kLane[k & 3u] + 8u - w * (it % per_word + 1u);
-            code |= ((word >> sh) & ((1u << w) - 1u)) << low;
+    uint32_t x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = 0u;
+    int low = bits;
+    for (int sg = 0; sg < sd.nseg; ++sg) {
+        const int w = sd.width[sg];
+        low -= w;
+        switch (w) {
+            case 1: unpack_segment<1>(x, low, sd.stream[sg], t, tile); break;
+            case 2: unpack_segment<2>(x, low, sd.stream[sg], t, tile); break;
+            case 4: unpack_segment<4>(x, low, sd.stream[sg], t, tile); break;
+            default: break;
         }
-        uint32_t rr, cc;
-        code_rc(t, k, rr, cc);
-        ts[rr * 64u + cc] = static_cast<uint8_t>(code);
+    }
+#pragma unroll
+    for (uint32_t it = 0; it < 32u; ++it) {
+        const uint32_t s = it >> 3, ch = (it >> 1) & 3u, ph = it & 1u;
+        const uint32_t rr = 16u * ch + t / 4u, cc = 16u * s + 8u * ph + 2u * (t % 4u);
+        uint32_t a, b;
+        asm("prmt.b32 %0, %1, 0, 0x4431;" : "=r"(a) : "r"(x[it]));  // lanes 1, 3 -> row rr
+        asm("prmt.b32 %0, %1, 0, 0x4420;" : "=r"(b) : "r"(x[it]));  // lanes 0, 2 -> row rr + 8
+        *reinterpret_cast<uint16_t*>(ts + rr * kTileStride + cc) = static_cast<uint16_t>(a);
+        *reinterpret_cast<uint16_t*>(ts + (rr + 8u) * kTileStride + cc) = static_cast<uint16_t>(b);
     }
     __syncwarp();
 #pragma unroll
@@ -300,7 +483,7 @@ __global__ void __launch_bounds__(32 * kPackWarps) unpack_kernel(uint8_t* __rest
         const uint32_t chunk = i * 32u + t;
         const uint32_t rr = chunk >> 2, cc = (chunk & 3u) * 16u;
         *reinterpret_cast<uint4*>(codes + static_cast<size_t>(r0 + rr) * cols_p + c0 + cc) =
-            *reinterpret_cast<const uint4*>(ts + rr * 64u + cc);
+            *reinterpret_cast<const uint4*>(ts + rr * kTileStride + cc);
     }
 }
 
@@ -581,8 +764,8 @@ cudaError_t launch_prepack(const uint8_t* codes, uint32_t rows_p, uint32_t cols_
                            const int* widths, uint8_t* const* streams, cudaStream_t st) {
     const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
     if (ntiles == 0) return cudaSuccess;
-    prepack_kernel<<<(ntiles + kPackWarps - 1) / kPackWarps, 32 * kPackWarps, 0, st>>>(
-        codes, cols_p, ntiles, bits, make_sd(nseg, widths, streams));
+    const uint32_t blocks = std::min<uint32_t>((ntiles + kPackWarps - 1) / kPackWarps, 148u * 8u);
+    prepack_kernel<<<blocks, 32 * kPackWarps, 0, st>>>(codes, cols_p, ntiles, bits, make_sd(nseg, widths, streams));
     return cudaGetLastError();
 }
 

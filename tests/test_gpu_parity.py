@@ -766,3 +766,50 @@ def test_x8_kernel_parity_subprocess(cuda):
                        cwd=ROOT)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("e,m", [(3, 2), (2, 3), (2, 2), (4, 3), (2, 1), (5, 2), (3, 1), (1, 1)])
+def test_quantize_exact_encode_decision_boundaries(cuda, oracle, e, m):
+    """The division-free encode (encode_exact in fpx_codec.cu) against the
+    reference's fp64 w / s encode at every decision boundary of the format:
+    each code value x s, each midpoint x s (exact ties), and the fp32
+    neighbours of every midpoint, both signs, for row scales from fp16
+    subnormal to large -- fp32 and fp16 input, two-step and fused paths."""
+    fpx = _fpx()
+    L = fpx._lib.load()
+    maxrep = float(L.fpx_max_representable(e, m))
+    cmax = 2 ** (e + m) - 1
+    vals = np.array([oracle.decode(i, e, m) for i in range(cmax + 1)], dtype=np.float64)
+    mids = ((vals[:-1] + vals[1:]) / 2).astype(np.float32)
+    rng = np.random.default_rng(100 * e + m)
+    rows = []
+    bias = 2 ** (e - 1) - 1
+    amax_limit = 0.9 * maxrep * 65504.0 / 2.0 ** (15 - bias)  # finite effective scale (codec.cpp:155-164)
+    for amax in [a for a in [3e-8, 1e-6, 4e-5, 1e-3, 0.0123, 0.7, 3.0, 97.0, 1500.0] if a < amax_limit]:
+        s = np.float32(np.float16(np.float32(np.float64(amax) / maxrep)))
+        if s == 0:
+            s = np.float32(2.0 ** -24)  # the reference bumps a zero scale to the smallest subnormal
+        cand = [np.float32(v) * s for v in vals.astype(np.float32)] + list(mids * s)
+        cand += list(np.nextafter(mids * s, np.float32(np.inf))) + list(np.nextafter(mids * s, np.float32(0)))
+        cand += list((rng.random(64) * amax).astype(np.float32))
+        cand = np.array([c for c in cand if abs(c) <= amax], dtype=np.float32)
+        cand *= rng.choice(np.array([-1, 1], dtype=np.float32), size=cand.size)
+        rows.append(np.concatenate([[np.float32(amax)], cand]))
+    width = max(r.size for r in rows)
+    w = np.zeros((len(rows), width), dtype=np.float32)
+    for i, r in enumerate(rows):
+        w[i, :r.size] = r
+    fmt = fpx.FpxFormat(e, m)
+    for dt in (torch.float32, torch.float16):
+        wt = torch.from_numpy(w).to(cuda).to(dt)
+        w_ref = wt.float().cpu().numpy()  # what the reference sees (to_fp32 of the fp16 input, codec.cpp:35-40)
+        st, codes, scales, _ = oracle.quantize(w_ref, e, m)
+        assert st == 0
+        q = fpx.quantize_matrix(wt, fmt)
+        assert (q.scales.cpu().numpy().view(np.uint16) == scales).all()
+        got = q.codes.cpu().numpy()
+        bad = np.argwhere(got != codes)
+        assert bad.size == 0, f"{dt} first mismatch at {bad[0]}: w={w_ref[tuple(bad[0])]!r} gpu={got[tuple(bad[0])]} ref={codes[tuple(bad[0])]}"
+        fused = fpx.quantize_pack(wt, fmt)
+        st, streams = oracle.pack(codes, scales, e, m)
+        assert all((a.cpu().numpy() == b).all() for a, b in zip(fused.streams, streams))
