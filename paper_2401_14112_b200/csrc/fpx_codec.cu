@@ -62,6 +62,43 @@ __device__ __forceinline__ uint32_t encode_exact(float w, float sv, float inv, i
     return sign | min(c, cmax);
 }
 
+// Four weights at once.  For the FP6 formats the candidate comes from the
+// sm_100a hardware conversion (cvt.rn.satfinite.e3m2x2 / e2m3x2.f32, two
+// codes per instruction) applied to q * (1 + 2^-20) and q * (1 - 2^-20):
+// where both agree no rounding boundary lies within 2^-20 of q -- wider than
+// q's own error -- so that is the reference's code; otherwise (near a tie,
+// rare) encode_exact decides.
+enum EncMode { kEncGeneric = 0, kEncHwE3M2 = 1, kEncHwE2M3 = 2 };
+
+template <int MODE>
+__device__ __forceinline__ uint32_t cvt_fp6x2(float lo, float hi) {
+    uint16_t r;
+    if constexpr (MODE == kEncHwE3M2)
+        asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    else
+        asm("cvt.rn.satfinite.e2m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+template <int MODE>
+__device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e, int m, int bias, uint32_t cmax) {
+    if constexpr (MODE == kEncGeneric) {
+        return encode_exact(v.x, sv, inv, e, m, bias, cmax) | encode_exact(v.y, sv, inv, e, m, bias, cmax) << 8 |
+               encode_exact(v.z, sv, inv, e, m, bias, cmax) << 16 | encode_exact(v.w, sv, inv, e, m, bias, cmax) << 24;
+    } else {
+        const float qa = fabsf(v.x) * inv, qb = fabsf(v.y) * inv, qc = fabsf(v.z) * inv, qd = fabsf(v.w) * inv;
+        constexpr float kUp = 1.0f + 0x1p-20f, kDn = 1.0f - 0x1p-20f;
+        const uint32_t up = cvt_fp6x2<MODE>(qa * kUp, qb * kUp) | cvt_fp6x2<MODE>(qc * kUp, qd * kUp) << 16;
+        const uint32_t dn = cvt_fp6x2<MODE>(qa * kDn, qb * kDn) | cvt_fp6x2<MODE>(qc * kDn, qd * kDn) << 16;
+        if (up != dn)  // a quotient near a rounding boundary
+            return encode4<kEncGeneric>(v, sv, inv, e, m, bias, cmax);
+        const uint32_t sgn = ((__float_as_uint(v.x) >> 31) | (__float_as_uint(v.y) >> 31) << 8 |
+                              (__float_as_uint(v.z) >> 31) << 16 | (__float_as_uint(v.w) >> 31) << 24)
+                             << 5;
+        return (up & 0x1f1f1f1fu) | sgn;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ float load_w(const T* p);
 template <>
@@ -95,10 +132,24 @@ __device__ __forceinline__ float4 load_w4<uint16_t>(const uint16_t* p, bool vec)
     return make_float4(a.x, a.y, b.x, b.y);
 }
 
+// 16 bytes of a row (16-byte aligned) as groups of 4 weights.
+__device__ __forceinline__ void load_w16(const float* p, float4 (&v)[1]) {
+    v[0] = __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void load_w16(const uint16_t* p, float4 (&v)[2]) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+    const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+    v[0] = make_float4(a.x, a.y, b.x, b.y);
+    v[1] = make_float4(c.x, c.y, d.x, d.y);
+}
+
 // Row pass: scale + status (+ the row's codes when codes != nullptr).
 // codes == nullptr: row scales, status and the per-row skip flag only (pass 1
 // of the fused quantize+pack, whose tile kernel encodes and packs).
-template <typename T>
+template <typename T, int MODE>
 __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, uint32_t rows,
                                                        uint32_t cols, uint32_t cols_p, int e, int m,
                                                        double maxrep, uint8_t* __restrict__ codes,
@@ -131,8 +182,35 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
     bool nan = false;
     // eight independent vector loads in flight per thread (the row is
     // streamed once here and once more, mostly from L2, by the encode)
+    // 16-byte loads (kG groups of 4 weights) when the rows are 16-byte aligned
+    constexpr uint32_t kG = 16u / (4u * sizeof(T));
+    const bool vec16 = (reinterpret_cast<uintptr_t>(w) % 16u) == 0 && (static_cast<size_t>(cols) * sizeof(T)) % 16u == 0;
     constexpr uint32_t kU = 8;
     uint32_t c = threadIdx.x * 4;
+    if (vec16 && kG > 1) {
+        const uint32_t stp = blockDim.x * 4 * kG;
+        for (c = threadIdx.x * 4 * kG; c + (kU / kG - 1) * stp + 4 * kG <= c4; c += (kU / kG) * stp) {
+            float4 v[kU / kG][kG];
+#pragma unroll
+            for (uint32_t u = 0; u < kU / kG; ++u) load_w16(row + c + u * stp, v[u]);
+#pragma unroll
+            for (uint32_t u = 0; u < kU / kG; ++u)
+#pragma unroll
+                for (uint32_t gq = 0; gq < kG; ++gq) {
+                    const float4 x = v[u][gq];
+                    nan |= isnan(x.x) | isnan(x.y) | isnan(x.z) | isnan(x.w);
+                    amax = fmaxf(fmaxf(amax, fmaxf(fabsf(x.x), fabsf(x.y))), fmaxf(fabsf(x.z), fabsf(x.w)));
+                }
+        }
+        // the rest 4 at a time, continuing where each thread's 16-byte walk stopped
+        for (uint32_t cq = c; cq < c4; cq += stp)
+            for (uint32_t gq = 0; gq < kG && cq + 4 * gq < c4; ++gq) {
+                const float4 x = load_w4(row + cq + 4 * gq, vec);
+                nan |= isnan(x.x) | isnan(x.y) | isnan(x.z) | isnan(x.w);
+                amax = fmaxf(fmaxf(amax, fmaxf(fabsf(x.x), fabsf(x.y))), fmaxf(fabsf(x.z), fabsf(x.w)));
+            }
+        c = c4;
+    }
     for (; c + (kU - 1) * blockDim.x * 4 < c4; c += kU * blockDim.x * 4) {
         float4 v[kU];
 #pragma unroll
@@ -208,11 +286,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
             for (uint32_t u = 0; u < kE; ++u) v[u] = load_w4(row + c0 + u * step, vec);
 #pragma unroll
             for (uint32_t u = 0; u < kE; ++u) {
-                const uint32_t packed = encode_exact(v[u].x, sv, inv, e, m, bias, cmax) |
-                                        encode_exact(v[u].y, sv, inv, e, m, bias, cmax) << 8 |
-                                        encode_exact(v[u].z, sv, inv, e, m, bias, cmax) << 16 |
-                                        encode_exact(v[u].w, sv, inv, e, m, bias, cmax) << 24;
-                *reinterpret_cast<uint32_t*>(out + c0 + u * step) = packed;
+                *reinterpret_cast<uint32_t*>(out + c0 + u * step) = encode4<MODE>(v[u], sv, inv, e, m, bias, cmax);
             }
         }
     }
@@ -358,7 +432,7 @@ __global__ void __launch_bounds__(32 * kPackWarps) prepack_kernel(const uint8_t*
 // straight from the weights (encode_exact with the row scales and skip flags
 // of pass 1) into shared memory, then packs them exactly like
 // prepack_kernel.  The code matrix never touches HBM.
-template <typename T>
+template <typename T, int MODE>
 __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T* __restrict__ w, uint32_t rows,
                                                                         uint32_t cols, uint32_t cols_p,
                                                                         uint32_t ntiles, int e, int m,
@@ -376,50 +450,60 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
     const int bias = (1 << (e - 1)) - 1;
     const uint32_t cmax = (1u << (e + m)) - 1u;
     (void)maxrep;
-    // two rows per pass: lanes 0-15 row 2i, 16-31 row 2i+1, the same 4
-    // consecutive columns every pass.  Passes in chunks of 8 with every load
-    // of the chunk issued first (the loads depend only on indices; row scales
-    // and skip flags load alongside and apply after).
-    const uint32_t cc = (t & 15u) * 4u, c = c0 + cc;
-    const bool full = c + 4u <= cols;
+    // Each lane reads 16 bytes of one row per pass -- kG groups of 4 weights
+    // (fp32: 1, fp16: 2) -- so kLpr lanes cover a 64-weight tile row and a
+    // pass covers kRpp rows; passes run in chunks with every load of the
+    // chunk issued first (loads depend only on indices; row scales and skip
+    // flags load alongside and apply after).
+    constexpr uint32_t kG = 16u / (4u * sizeof(T)), kLpr = 16u / kG, kRpp = 32u / kLpr;
+    constexpr uint32_t kChunk = 8u / kG;
+    const uint32_t cc = (t % kLpr) * 4u * kG, c = c0 + cc;
+    const bool full = c + 4u * kG <= cols;
     const bool vec = (reinterpret_cast<uintptr_t>(w) % 16u) == 0 && (static_cast<size_t>(cols) * sizeof(T)) % 16u == 0;
-    constexpr uint32_t kChunk = 8;
 #pragma unroll 1
-    for (uint32_t i0 = 0; i0 < 32u; i0 += kChunk) {
-        float4 v[kChunk];
+    for (uint32_t i0 = 0; i0 < 64u / kRpp; i0 += kChunk) {
+        float4 v[kChunk][kG];
         uint16_t sraw[kChunk];
         uint8_t skip[kChunk];
 #pragma unroll
         for (uint32_t j = 0; j < kChunk; ++j) {
-            const uint32_t r = r0 + 2u * (i0 + j) + (t >> 4);
-            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint32_t r = r0 + kRpp * (i0 + j) + t / kLpr;
+#pragma unroll
+            for (uint32_t gq = 0; gq < kG; ++gq) v[j][gq] = make_float4(0.f, 0.f, 0.f, 0.f);
             sraw[j] = 0x3c00u;
             skip[j] = 1;
             if (r < rows) {
                 const T* row = w + static_cast<size_t>(r) * cols;
                 sraw[j] = scales[r];
                 skip[j] = row_skip[r];
-                if (full) {
-                    v[j] = load_w4(row + c, vec);
-                } else if (c < cols) {
-                    v[j].x = load_w(row + c);
-                    if (c + 1 < cols) v[j].y = load_w(row + c + 1);
-                    if (c + 2 < cols) v[j].z = load_w(row + c + 2);
+                if (full && vec) {
+                    load_w16(row + c, v[j]);
+                } else {
+#pragma unroll
+                    for (uint32_t q = 0; q < 4u * kG; ++q) {
+                        const float x = c + q < cols ? load_w(row + c + q) : 0.0f;
+                        float* f = reinterpret_cast<float*>(&v[j][q / 4]);
+                        f[q % 4] = x;
+                    }
                 }
             }
         }
 #pragma unroll
         for (uint32_t j = 0; j < kChunk; ++j) {
-            const uint32_t rr = 2u * (i0 + j) + (t >> 4);
-            uint32_t packed4 = 0;
+            const uint32_t rr = kRpp * (i0 + j) + t / kLpr;
+            uint32_t packed[kG];
+#pragma unroll
+            for (uint32_t gq = 0; gq < kG; ++gq) packed[gq] = 0u;
             if (!skip[j]) {
                 const float sv = __half2float(__ushort_as_half(sraw[j])), inv = __frcp_rn(sv);
-                const float vv[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
-                for (uint32_t q = 0; q < 4u; ++q)
-                    if (c + q < cols) packed4 |= encode_exact(vv[q], sv, inv, e, m, bias, cmax) << (8u * q);
+                for (uint32_t gq = 0; gq < kG; ++gq)  // columns >= cols hold +0.0: code 0
+                    packed[gq] = encode4<MODE>(v[j][gq], sv, inv, e, m, bias, cmax);
             }
-            *reinterpret_cast<uint32_t*>(ts + rr * kTileStride + cc) = packed4;
+            if constexpr (kG == 1)
+                *reinterpret_cast<uint32_t*>(ts + rr * kTileStride + cc) = packed[0];
+            else
+                *reinterpret_cast<uint2*>(ts + rr * kTileStride + cc) = make_uint2(packed[0], packed[kG - 1]);
         }
     }
     __syncwarp();
@@ -725,16 +809,63 @@ static SplitDescC make_sdc(int nseg, const int* widths, const uint8_t* const* st
     return sd;
 }
 
+static int enc_mode(int e, int m) { return e == 3 && m == 2 ? kEncHwE3M2 : (e == 2 && m == 3 ? kEncHwE2M3 : kEncGeneric); }
+
+template <typename T, int MODE>
+static void launch_quantize_t(const void* w, uint32_t rows, uint32_t cols, uint32_t rows_p, uint32_t cols_p, int e,
+                              int m, double maxrep, uint8_t* codes, uint16_t* scales, unsigned long long* status,
+                              uint8_t* row_skip, cudaStream_t st) {
+    quantize_kernel<T, MODE><<<rows_p, 256, 0, st>>>(static_cast<const T*>(w), rows, cols, cols_p, e, m, maxrep, codes,
+                                                     scales, status, row_skip);
+}
+
+template <typename T>
+static void launch_quantize_m(const void* w, uint32_t rows, uint32_t cols, uint32_t rows_p, uint32_t cols_p, int e,
+                              int m, double maxrep, uint8_t* codes, uint16_t* scales, unsigned long long* status,
+                              uint8_t* row_skip, cudaStream_t st) {
+    // the mode only matters for the encode (codes != nullptr)
+    switch (codes == nullptr ? kEncGeneric : enc_mode(e, m)) {
+        case kEncHwE3M2:
+            return launch_quantize_t<T, kEncHwE3M2>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status,
+                                                    row_skip, st);
+        case kEncHwE2M3:
+            return launch_quantize_t<T, kEncHwE2M3>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status,
+                                                    row_skip, st);
+        default:
+            return launch_quantize_t<T, kEncGeneric>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales,
+                                                     status, row_skip, st);
+    }
+}
+
 cudaError_t launch_quantize(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
                             uint32_t cols_p, int e, int m, double maxrep, uint8_t* codes,
                             uint16_t* scales, unsigned long long* status, cudaStream_t st) {
     if (w_dtype == 0)
-        quantize_kernel<float><<<rows_p, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, cols_p, e, m,
-                                                       maxrep, codes, scales, status, nullptr);
+        launch_quantize_m<float>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status, nullptr, st);
     else
-        quantize_kernel<uint16_t><<<rows_p, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, cols_p,
-                                                          e, m, maxrep, codes, scales, status, nullptr);
+        launch_quantize_m<uint16_t>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status, nullptr, st);
     return cudaGetLastError();
+}
+
+template <typename T>
+static void launch_qpack(const void* w, uint32_t rows, uint32_t cols, uint32_t cols_p, uint32_t ntiles, int e, int m,
+                         double maxrep, const uint16_t* scales, const uint8_t* row_skip, int bits, const SplitDesc& sd,
+                         cudaStream_t st) {
+    const uint32_t grid = (ntiles + kPackWarps - 1) / kPackWarps;
+    const T* wt = static_cast<const T*>(w);
+    switch (enc_mode(e, m)) {
+        case kEncHwE3M2:
+            quantize_pack_kernel<T, kEncHwE3M2><<<grid, 32 * kPackWarps, 0, st>>>(wt, rows, cols, cols_p, ntiles, e, m,
+                                                                                 maxrep, scales, row_skip, bits, sd);
+            break;
+        case kEncHwE2M3:
+            quantize_pack_kernel<T, kEncHwE2M3><<<grid, 32 * kPackWarps, 0, st>>>(wt, rows, cols, cols_p, ntiles, e, m,
+                                                                                 maxrep, scales, row_skip, bits, sd);
+            break;
+        default:
+            quantize_pack_kernel<T, kEncGeneric><<<grid, 32 * kPackWarps, 0, st>>>(wt, rows, cols, cols_p, ntiles, e, m,
+                                                                                  maxrep, scales, row_skip, bits, sd);
+    }
 }
 
 cudaError_t launch_quantize_pack(const void* w, int w_dtype, uint32_t rows, uint32_t cols, uint32_t rows_p,
@@ -744,18 +875,12 @@ cudaError_t launch_quantize_pack(const void* w, int w_dtype, uint32_t rows, uint
     const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
     const int bits = 1 + e + m;
     const SplitDesc sd = make_sd(nseg, widths, streams);
-    const uint32_t grid = (ntiles + kPackWarps - 1) / kPackWarps;
     if (w_dtype == 0) {
-        quantize_kernel<float><<<rows_p, 256, 0, st>>>(static_cast<const float*>(w), rows, cols, cols_p, e, m,
-                                                       maxrep, nullptr, scales, status, row_skip);
-        quantize_pack_kernel<float><<<grid, 32 * kPackWarps, 0, st>>>(
-            static_cast<const float*>(w), rows, cols, cols_p, ntiles, e, m, maxrep, scales, row_skip, bits, sd);
+        launch_quantize_m<float>(w, rows, cols, rows_p, cols_p, e, m, maxrep, nullptr, scales, status, row_skip, st);
+        launch_qpack<float>(w, rows, cols, cols_p, ntiles, e, m, maxrep, scales, row_skip, bits, sd, st);
     } else {
-        quantize_kernel<uint16_t><<<rows_p, 256, 0, st>>>(static_cast<const uint16_t*>(w), rows, cols, cols_p, e,
-                                                          m, maxrep, nullptr, scales, status, row_skip);
-        quantize_pack_kernel<uint16_t><<<grid, 32 * kPackWarps, 0, st>>>(static_cast<const uint16_t*>(w), rows,
-                                                                         cols, cols_p, ntiles, e, m, maxrep,
-                                                                         scales, row_skip, bits, sd);
+        launch_quantize_m<uint16_t>(w, rows, cols, rows_p, cols_p, e, m, maxrep, nullptr, scales, status, row_skip, st);
+        launch_qpack<uint16_t>(w, rows, cols, cols_p, ntiles, e, m, maxrep, scales, row_skip, bits, sd, st);
     }
     return cudaGetLastError();
 }
