@@ -808,26 +808,44 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&accempty[ab]);
             if (q == 0 && lane == 0) trace_cta(p, 1 + lu);
-            if (p.split > 1) {
-                __threadfence();
-                __syncwarp();
-                uint32_t old = 0;
-                if (lane == 0) old = atomicAdd(&p.counters[mt * 4 + q], 1u);
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == p.split - 1 && ndefer < kMaxDefer) {
-                    // last arriver of this (tile, quarter): defer the reduction to the
-                    // CTA-wide pass after the main loop (final_split_reduce)
-                    __threadfence();  // acquire side of the counter (the other chunks' partials)
-                    if (lane == 0) {
-                        red_tq[q * kMaxDefer + ndefer] = mt * 4 + q;
-                        p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
+        }
+        if (p.split > 1) {
+            // Split-K arrivals for all of the CTA's chunks at once, after its
+            // last unit: one release fence per epilogue warp instead of one
+            // per unit (a MEMBAR under full HBM load stalls the warp for
+            // microseconds, and the accumulator it holds stalls the MMA two
+            // units later).  The last arriver of a (tile, quarter) reduces it
+            // in the CTA-wide pass after the main loop (final_split_reduce),
+            // or here when its deferral list is full.
+            __threadfence();
+            __syncwarp();
+            bool acquired = false;
+            // lane i arrives for the CTA's unit ub + i: one atomic round trip per 32 units
+            for (uint32_t ub = u_begin; ub < u_end; ub += 32) {
+                const uint32_t u = ub + lane;
+                uint32_t mt = 0, ch, s0, ns;
+                bool last = false;
+                if (u < u_end) {
+                    unit_of(u, mt, ch, s0, ns);
+                    last = atomicAdd(&p.counters[mt * 4 + q], 1u) == p.split - 1;
+                }
+                uint32_t lasts = __ballot_sync(0xffffffffu, last);
+                if (lasts != 0u && !acquired) {
+                    __threadfence();  // acquire side of the counters (the other chunks' partials)
+                    acquired = true;
+                }
+                if (last) p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
+                while (lasts != 0u) {
+                    const uint32_t i = __ffs(lasts) - 1;
+                    lasts &= lasts - 1;
+                    const uint32_t mti = __shfl_sync(0xffffffffu, mt, i);
+                    if (ndefer < kMaxDefer) {
+                        if (lane == 0) red_tq[q * kMaxDefer + ndefer] = mti * 4 + q;
+                        ++ndefer;
+                    } else {
+                        const uint32_t m = mti * kTileM + row_l;
+                        split_reduce_rows<NPAD>(p, mti, row_l, m, m < p.rows_p);
                     }
-                    ++ndefer;
-                } else if (old == p.split - 1) {
-                    // deferral list full (more than kMaxDefer units per CTA): reduce here
-                    __threadfence();
-                    split_reduce_rows<NPAD>(p, mt, row_l, m, row_ok);
-                    if (lane == 0) p.counters[mt * 4 + q] = 0;  // self-cleaning for the next launch
                 }
             }
         }

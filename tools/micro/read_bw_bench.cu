@@ -58,6 +58,65 @@ __global__ void __launch_bounds__(64) tma_read(TArgs a) {
     }
 }
 
+
+// The decode kernel's weight pattern: a CTA streams one unit (2 tile-rows x
+// a K chunk) of the hi (1 KB/tile) and lo (2 KB/tile) streams; a stage is
+// KS k-tiles: 4 bulk copies (hi r0, hi r1, lo r0, lo r1) of KS KB / 2 KS KB.
+struct PArgs {
+    const uint8_t* hi;
+    const uint8_t* lo;
+    int kt, tile_rows, split, ks, stages;
+    unsigned long long* sink;
+};
+__global__ void __launch_bounds__(64) pattern_read(PArgs a) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t full[32], empty[32];
+    const uint32_t warp = threadIdx.x >> 5;
+    const int stage_bytes = 6 * 1024 * a.ks;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < a.stages; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int units = a.tile_rows / 2 * a.split;
+    const int u0 = (int)((long)blockIdx.x * units / gridDim.x), u1 = (int)((long)(blockIdx.x + 1) * units / gridDim.x);
+    const uint64_t pol = policy_evict_first();
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t i = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int mt = u / a.split, ch = u % a.split;
+                const int k0 = ch * a.kt / a.split, k1 = (ch + 1) * a.kt / a.split;
+                for (int k = k0; k + a.ks <= k1; k += a.ks, ++i) {
+                    const uint32_t s = i % a.stages, ph = (i / a.stages) & 1u;
+                    if (i >= (uint32_t)a.stages) mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    uint8_t* d = sm + (size_t)s * stage_bytes;
+                    for (int r = 0; r < 2; ++r) {
+                        const size_t t = (size_t)(2 * mt + r) * a.kt + k;
+                        bulk_g2s(d + r * 1024 * a.ks, a.hi + t * 1024, 1024 * a.ks, &full[s], pol);
+                        bulk_g2s(d + 2048 * a.ks + r * 2048 * a.ks, a.lo + t * 2048, 2048 * a.ks, &full[s], pol);
+                    }
+                }
+            }
+        }
+    } else {
+        uint32_t i = 0, acc = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int ch = u % a.split;
+            const int k0 = ch * a.kt / a.split, k1 = (ch + 1) * a.kt / a.split;
+            for (int k = k0; k + a.ks <= k1; k += a.ks, ++i) {
+                const uint32_t s = i % a.stages, ph = (i / a.stages) & 1u;
+                mbar_wait(&full[s], ph);
+                acc ^= lds32(smem_u32(sm + (size_t)s * stage_bytes + 4 * (threadIdx.x & 31)));
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+            }
+        }
+        if (acc == 0x12345679u) atomicAdd(a.sink, 1ull);
+    }
+}
+
 __global__ void __launch_bounds__(512) ldg_read(const uint4* __restrict__ src, size_t nvec,
                                                 unsigned long long* sink) {
     const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
@@ -156,6 +215,28 @@ int main() {
         printf("LDG %d CTA/SM x 512 thr x 8 x 16 B: 2 GiB %7.1f us = %6.0f GB/s | 135 MB b2b %5.1f us = %6.0f GB/s\n", bps,
                ub, big / ub / 1e3, us, small / us / 1e3);
         CK(cudaGetLastError());
+    }
+    // the decode kernel's access pattern, 8192 x 22016 e3m2 (hi 45 MB, lo 90 MB, 3 rotated copies)
+    {
+        const int kt = 344, trs = 128;
+        const size_t hi_b = (size_t)trs * kt * 1024, lo_b = (size_t)trs * kt * 2048;
+        uint8_t* pbuf;
+        CK(cudaMalloc(&pbuf, 3 * (hi_b + lo_b)));
+        CK(cudaMemset(pbuf, 1, 3 * (hi_b + lo_b)));
+        struct PC { int grid, split, ks, stages; };
+        for (PC c : {PC{128, 2, 2, 13}, PC{128, 2, 2, 17}, PC{148, 9, 2, 13}, PC{128, 2, 4, 7}, PC{128, 2, 1, 26}, PC{148, 37, 2, 13}}) {
+            const int smem = c.stages * 6 * 1024 * c.ks;
+            if (cudaFuncSetAttribute(pattern_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) continue;
+            auto l = [&](int r) {
+                const uint8_t* base = pbuf + (r % 3) * (hi_b + lo_b);
+                PArgs a{base, base + hi_b, kt, trs, c.split, c.ks, c.stages, sink};
+                pattern_read<<<c.grid, 64, smem>>>(a);
+            };
+            const double us = time_it(l, 12);
+            printf("pattern grid %3d split %2d KS %d stages %2d (%3d KB ring): 135 MB b2b %5.1f us = %6.0f GB/s\n", c.grid,
+                   c.split, c.ks, c.stages, smem / 1024, us, (hi_b + lo_b) / us / 1e3);
+            CK(cudaGetLastError());
+        }
     }
     printf("done\n");
     return 0;
