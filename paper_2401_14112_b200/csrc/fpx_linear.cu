@@ -451,7 +451,19 @@ struct GCfg {
     static constexpr int kLoOff = 2 * kKS * kHiBytes;
     static constexpr int kWStageBytes = (2 * kKS * (kHiBytes + kLoBytes) + 1023) / 1024 * 1024;
     static constexpr int kBStageBytes = (kKS * kBBytes + 1023) / 1024 * 1024;
-    static constexpr int kAccCol0 = int(kTmemCols) - 2 * NPAD;  // double-buffered accumulator at the top
+    // Wide batches (NPAD >= 64): the MMA warp itself waits for each stage's
+    // activations, so the activation ring (16-32 KB stages) need not be as
+    // deep as the A-slot ring, and one accumulator buffer leaves TMEM for
+    // more A slots (a CTA runs one long unit at the default splits; a
+    // second unit waits for the epilogue to drain the first).  Narrow
+    // batches keep the de-quantisers' activation wait (one MMA-loop wait
+    // less) and double-buffered accumulators.
+    static constexpr bool kMmaWaitsB = NPAD >= 64;
+#ifndef FPX_DEC_WIDE_ACCBUFS
+#define FPX_DEC_WIDE_ACCBUFS 2
+#endif
+    static constexpr int kAccBufs = NPAD >= 64 ? FPX_DEC_WIDE_ACCBUFS : 2;
+    static constexpr int kAccCol0 = int(kTmemCols) - kAccBufs * NPAD;  // accumulator buffer(s) at the top
     static constexpr int kASlotsMax = (kAccCol0 / 32) / kKS;      // A stage slots the TMEM budget allows
 #ifndef FPX_DEC_SB
 #define FPX_DEC_SB 12
@@ -460,10 +472,10 @@ struct GCfg {
 #define FPX_DEC_SB32 FPX_DEC_SB
 #endif
 #ifndef FPX_DEC_SB64
-#define FPX_DEC_SB64 6
+#define FPX_DEC_SB64 4
 #endif
 #ifndef FPX_DEC_SB128
-#define FPX_DEC_SB128 4
+#define FPX_DEC_SB128 3
 #endif
 #ifndef FPX_DEC_SMEM_KB
 #define FPX_DEC_SMEM_KB 216
@@ -483,11 +495,15 @@ struct GCfg {
     // TMEM A stage slots, at most the activation ring's depth and the weight
     // ring's depth minus the groups (see the SB >= R and SW >= G + R
     // assertions below).
-    static constexpr int kASlots = std::min(std::min(kASlotsMax, kBStages), kWStages - kG);
+    static constexpr int kASlots = std::min(std::min(kASlotsMax, kMmaWaitsB ? 16 : kBStages), kWStages - kG);
 #ifndef FPX_DEC_BS
 #define FPX_DEC_BS 3
 #endif
-    static constexpr int kBS = std::max(1, std::min(FPX_DEC_BS, kASlots / 2));  // stages per commit batch
+    // stages per commit batch; with R >= G + BS a group never waits for the
+    // batch holding its own previous stage (R = 6, G = 3 or 4 at NPAD 64 /
+    // 128 takes BS = 2)
+    static constexpr int kBS =
+        std::max(1, std::min(std::min(std::min(FPX_DEC_BS, kASlots / 2), std::max(1, kASlots - kG)), kBStages - 1));
     static constexpr int kNB = (std::max(kBStages, kASlots) + kBS - 1) / kBS + 3;  // batch barriers (no aliasing)
     static constexpr int kBarBytes = 8 * (2 * kWStages + kBStages + kNB + kASlots + 5) + 16;
     static constexpr int kSmemBytes = kWStages * kWStageBytes + kBStages * kBStageBytes + kBarBytes + 1024;
@@ -500,7 +516,7 @@ struct GCfg {
     // MMA consumed it, which freed this group's A slot).  Hence SB >= R.
     // (SB < R let a group pass the wait on the slot's older phase: wrong
     // results with SB=6, faults with smaller rings.)
-    static_assert(kBStages >= kASlots, "activation ring must be at least as deep as the A-slot ring");
+    static_assert(kMmaWaitsB || kBStages >= kASlots, "activation ring must be at least as deep as the A-slot ring");
     // The same argument for the weight ring: a group waits wfull for stage si
     // right after finishing its stage si - G, whose A slot required the MMA to
     // have consumed stage si - G - R -- so every stage up to there has landed.
@@ -689,16 +705,20 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         uint32_t bsl = 0;           // activation slot
         uint32_t nb = 0, nbs = 0;   // stages in the open commit batch, batch barrier slot
         uint32_t nbatch = 0;        // batch commits issued
+        uint32_t bph = 0;           // activation slot parity (kMmaWaitsB)
         for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
             uint32_t mt, ch, s0, ns;
             unit_of(u, mt, ch, s0, ns);
-            const uint32_t ab = lu & 1u;
-            wait_rec(p, &accempty[ab], ((lu >> 1) & 1u) ^ 1u, 5, lu);  // epilogue done with unit lu-2
+            constexpr uint32_t AB = C::kAccBufs;
+            const uint32_t ab = lu % AB;
+            wait_rec(p, &accempty[ab], ((lu / AB) & 1u) ^ 1u, 5, lu);  // epilogue done with unit lu - AB
             tc_fence_after();
             const uint32_t d_tmem = tmem + C::kAccCol0 + ab * NPAD;
             for (uint32_t ls = 0; ls < ns; ++ls, ++si) {
                 if (leader) trace_mark(p, kTrMmaWait, si);
-                // aready implies the activation stage landed (the group waited bfull first)
+                // narrow batches: aready implies the activation stage landed (the
+                // group waited bfull first); wide batches wait for it here
+                if constexpr (C::kMmaWaitsB) wait_rec(p, &bfull[bsl], bph, 8, si);
                 wait_rec(p, &aready[as], aph, 4, si);
                 tc_fence_after();
                 if (leader) trace_mark(p, kTrMmaGo, si);
@@ -723,7 +743,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                 }
                 if (leader) trace_mark(p, kTrMmaIssued, si);
                 if (++as == static_cast<uint32_t>(R)) as = 0, aph ^= 1u;
-                if (++bsl == static_cast<uint32_t>(SB)) bsl = 0;
+                if (++bsl == static_cast<uint32_t>(SB)) bsl = 0, bph ^= 1u;
             }
             umma_commit_warp(&accfull[ab]);
         }
@@ -757,8 +777,8 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         for (uint32_t u = u_begin; u < u_end; ++u, ++lu) {
             uint32_t mt, ch, s0, ns;
             unit_of(u, mt, ch, s0, ns);
-            const uint32_t ab = lu & 1u;
-            wait_rec(p, &accfull[ab], (lu >> 1) & 1u, 2, lu);
+            const uint32_t ab = lu % C::kAccBufs;
+            wait_rec(p, &accfull[ab], (lu / C::kAccBufs) & 1u, 2, lu);
             if (q == 0 && lane == 0) trace_mark(p, kTrEpiFull, lu);
             tc_fence_after();
             const uint32_t m = mt * kTileM + row_l;
@@ -951,7 +971,8 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
                     tmem_st_wait();
                     tc_fence_before();
                     // the MMA reads this stage's activations: make sure they landed
-                    wait_rec(p, &bfull[si % SB], (si / SB) & 1u, 8, si);
+                    // (wide batches: the MMA warp waits for them itself)
+                    if constexpr (!C::kMmaWaitsB) wait_rec(p, &bfull[si % SB], (si / SB) & 1u, 8, si);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&aready[as]);
                     if (q == 0 && lane == 0) trace_mark(p, kTrMmaAfull, si);
