@@ -74,7 +74,13 @@ def gather_output(c_local: torch.Tensor, rows_p: int, rank: int, world: int, gro
     padded = torch.zeros((n, m_slot), dtype=c_local.dtype, device=c_local.device)
     padded[:, :nrows[rank]] = c_local
     gathered = torch.empty((world * n, m_slot), dtype=c_local.dtype, device=c_local.device)
-    dist.all_gather_into_tensor(gathered, padded, group=group)  # rank-major concatenation
+    if padded.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo (CPU-side tests, several ranks sharing one GPU): stage through host memory
+        host = torch.empty((world * n, m_slot), dtype=c_local.dtype)
+        dist.all_gather_into_tensor(host, padded.cpu(), group=group)
+        gathered.copy_(host)
+    else:
+        dist.all_gather_into_tensor(gathered, padded, group=group)  # rank-major concatenation (NCCL over NVLink)
     out = torch.empty((n, rows_p), dtype=c_local.dtype, device=c_local.device)
     return permute(gathered.view(world, n, m_slot), row0, nrows, m_slot, n, out)
 

@@ -813,3 +813,55 @@ def test_quantize_exact_encode_decision_boundaries(cuda, oracle, e, m):
         fused = fpx.quantize_pack(wt, fmt)
         st, streams = oracle.pack(codes, scales, e, m)
         assert all((a.cpu().numpy() == b).all() for a, b in zip(fused.streams, streams))
+
+
+def _sharded_gpu_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    from paper_2401_14112_b200 import shard
+    fpx = _fpx()
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator(device=dev)
+        g.manual_seed(77)
+        w = torch.randn(1216, 2048, device=dev, generator=g) * 0.02  # 19 tile-rows: ragged shards
+        p = fpx.quantize_pack(w, fpx.FpxFormat.e3m2())
+        res = []
+        for n in (1, 16, 40):
+            b = torch.randn(n, 2048, device=dev, generator=g).half()
+            full = fpx.gemm_packed(p, b)  # the 1-GPU launch, same (full-problem) split
+            c = shard.sharded_linear(p, b, rank, world)  # shard kernel (C-ABI) + all-gather + fpx_gather_permute
+            torch.cuda.synchronize()
+            res.append(bool(torch.equal(c, full)))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_linear_multiprocess_c_abi_chain(cuda, world):
+    """world ranks (processes) on one GPU run the real C-ABI chain of the
+    column-sharded linear -- each rank's tile-row shard through fpx_linear,
+    the all-gather of the output slices (gloo here: NCCL refuses two ranks
+    on one device), fpx_gather_permute into col-major C -- and every rank's
+    assembled C is bit-identical to the single-launch result (ragged last
+    shard, N 1 / 16 / 40)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    for rank, oks in res:
+        assert all(oks), f"rank {rank}: sharded C differs from the 1-GPU launch: {oks}"
