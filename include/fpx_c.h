@@ -151,7 +151,10 @@ int fpx_dequantize(const uint8_t* const* streams, int nseg, const int* widths,
  * tile-row shard computed with the full problem's split_k is bit-identical
  * to the same rows of the unsharded result.
  * workspace: device buffer of >= fpx_linear_workspace_size(...) bytes
- * (never NULL: it always holds the 64 KiB split-K arrival-counter table),
+ * (never NULL: it always holds the 64 KiB split-K arrival-counter table;
+ * with FPX_LINEAR_X8=1 it also holds the activations' e4m3 split for the
+ * opt-in kind::f8f6f4 kernel at n <= 32, which runs only when the buffer is
+ * that large),
  * zero-filled once before first use; the counters self-clean after every
  * launch.  ONE WORKSPACE PER STREAM: two calls that may run concurrently
  * (distinct streams) must not share a workspace.  A call whose launch fails
