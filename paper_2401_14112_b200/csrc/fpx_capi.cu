@@ -68,6 +68,34 @@ int check_device(bool need_sm100) {
     return FPX_OK;
 }
 
+// Per-call status words and skip flags come from a stream-ordered pool the
+// library owns, one per device, that keeps its memory between calls (release
+// threshold = max).  The default pool returns everything at each
+// synchronisation, which made every cudaMallocAsync of a few bytes remap
+// memory: ~0.4 ms per quantize / prepack call on B200.
+static cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if (cudaError_t e = cudaMemPoolCreate(&pools[dev], &props)) return e;
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(ptr, bytes, pool, s);
+}
+
 int resolve_split(int e, int m, const int* widths, int nseg, int* w_out) {
     if (widths == nullptr || nseg == 0) {
         nseg = fpx_split_for_format(e, m, w_out);
@@ -300,7 +328,7 @@ int fpx_quantize(const void* w, int dtype, uint32_t rows, uint32_t cols, int e, 
     unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
     bool own = false;
     if (!status) {
-        FPX_CUDA(cudaMallocAsync(&status, sizeof(unsigned long long), s));
+        FPX_CUDA(scratch_alloc(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
         own = true;
     }
     FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
@@ -334,7 +362,7 @@ int fpx_dequantize_codes(const uint8_t* codes, const uint16_t* scales, uint32_t 
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
     const bool own = status == nullptr;
-    if (own) FPX_CUDA(cudaMallocAsync(&status, sizeof(unsigned long long), s));
+    if (own) FPX_CUDA(scratch_alloc(reinterpret_cast<void**>(&status), sizeof(unsigned long long), s));
     FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
     FPX_CUDA(launch_dequant_codes(codes, scales, rows_p, cols_p, e, m, status, w_f16, s));
     if (!own) return FPX_OK;
@@ -366,7 +394,7 @@ int fpx_quantize_pack(const void* w, int dtype, uint32_t rows, uint32_t cols, in
     unsigned long long* status = reinterpret_cast<unsigned long long*>(status_dev);
     uint8_t* scratch = nullptr;  // [status (own) | row skip flags]
     const size_t skip_off = 16;
-    FPX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), skip_off + rows_p, s));
+    FPX_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), skip_off + rows_p, s));
     const bool own = status == nullptr;
     if (own) status = reinterpret_cast<unsigned long long*>(scratch);
     FPX_CUDA(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), s));
@@ -405,7 +433,7 @@ int fpx_prepack(const uint8_t* codes, const uint16_t* scales, uint32_t rows_p, u
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (scales) {
         unsigned int* bad = nullptr;
-        FPX_CUDA(cudaMallocAsync(&bad, sizeof(unsigned int), s));
+        FPX_CUDA(scratch_alloc(reinterpret_cast<void**>(&bad), sizeof(unsigned int), s));
         FPX_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned int), s));
         FPX_CUDA(launch_check_scales(scales, rows_p, 15 - bias_of(e), bad, s));
         unsigned int hb = 0;

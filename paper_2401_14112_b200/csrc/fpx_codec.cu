@@ -68,12 +68,19 @@ __device__ __forceinline__ uint32_t encode_exact(float w, float sv, float inv, i
 // where both agree no rounding boundary lies within 2^-20 of q -- wider than
 // q's own error -- so that is the reference's code; otherwise (near a tie,
 // rare) encode_exact decides.
-enum EncMode { kEncGeneric = 0, kEncHwE3M2 = 1, kEncHwE2M3 = 2 };
+//
+// FP5 e2m2 rides on the e3m2 conversion: e2m2(q) = 4 * e3m2(q / 4) for
+// q / 4 <= 1.75.  Both keep 2 mantissa bits; e3m2's normal range starts at
+// 2^-2 (q >= 1, e2m2's normal range) with the same exponent field (bias 3
+// vs 1 absorbs the factor 4), and its subnormal step 2^-4 is e2m2's 2^-2 / 4.
+// So the e2m2 magnitude code is the e3m2 one, saturated at 15 (7.0) where
+// the quotient rounds to 2.0 or above.
+enum EncMode { kEncGeneric = 0, kEncHwE3M2 = 1, kEncHwE2M3 = 2, kEncHwE2M2 = 3 };
 
 template <int MODE>
 __device__ __forceinline__ uint32_t cvt_fp6x2(float lo, float hi) {
     uint16_t r;
-    if constexpr (MODE == kEncHwE3M2)
+    if constexpr (MODE == kEncHwE3M2 || MODE == kEncHwE2M2)
         asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
     else
         asm("cvt.rn.satfinite.e2m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
@@ -86,7 +93,9 @@ __device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e
         return encode_exact(v.x, sv, inv, e, m, bias, cmax) | encode_exact(v.y, sv, inv, e, m, bias, cmax) << 8 |
                encode_exact(v.z, sv, inv, e, m, bias, cmax) << 16 | encode_exact(v.w, sv, inv, e, m, bias, cmax) << 24;
     } else {
-        const float qa = fabsf(v.x) * inv, qb = fabsf(v.y) * inv, qc = fabsf(v.z) * inv, qd = fabsf(v.w) * inv;
+        constexpr bool k5 = MODE == kEncHwE2M2;
+        const float iv = k5 ? inv * 0.25f : inv;  // exact: a power-of-two factor
+        const float qa = fabsf(v.x) * iv, qb = fabsf(v.y) * iv, qc = fabsf(v.z) * iv, qd = fabsf(v.w) * iv;
         constexpr float kUp = 1.0f + 0x1p-20f, kDn = 1.0f - 0x1p-20f;
         const uint32_t up = cvt_fp6x2<MODE>(qa * kUp, qb * kUp) | cvt_fp6x2<MODE>(qc * kUp, qd * kUp) << 16;
         const uint32_t dn = cvt_fp6x2<MODE>(qa * kDn, qb * kDn) | cvt_fp6x2<MODE>(qc * kDn, qd * kDn) << 16;
@@ -94,7 +103,8 @@ __device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e
             return encode4<kEncGeneric>(v, sv, inv, e, m, bias, cmax);
         const uint32_t sgn = ((__float_as_uint(v.x) >> 31) | (__float_as_uint(v.y) >> 31) << 8 |
                               (__float_as_uint(v.z) >> 31) << 16 | (__float_as_uint(v.w) >> 31) << 24)
-                             << 5;
+                             << (k5 ? 4 : 5);
+        if constexpr (k5) return __vminu4(up & 0x1f1f1f1fu, 0x0f0f0f0fu) | sgn;
         return (up & 0x1f1f1f1fu) | sgn;
     }
 }
@@ -809,7 +819,11 @@ static SplitDescC make_sdc(int nseg, const int* widths, const uint8_t* const* st
     return sd;
 }
 
-static int enc_mode(int e, int m) { return e == 3 && m == 2 ? kEncHwE3M2 : (e == 2 && m == 3 ? kEncHwE2M3 : kEncGeneric); }
+static int enc_mode(int e, int m) {
+    if (e == 3 && m == 2) return kEncHwE3M2;
+    if (e == 2 && m == 3) return kEncHwE2M3;
+    return e == 2 && m == 2 ? kEncHwE2M2 : kEncGeneric;
+}
 
 template <typename T, int MODE>
 static void launch_quantize_t(const void* w, uint32_t rows, uint32_t cols, uint32_t rows_p, uint32_t cols_p, int e,
@@ -830,6 +844,9 @@ static void launch_quantize_m(const void* w, uint32_t rows, uint32_t cols, uint3
                                                     row_skip, st);
         case kEncHwE2M3:
             return launch_quantize_t<T, kEncHwE2M3>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status,
+                                                    row_skip, st);
+        case kEncHwE2M2:
+            return launch_quantize_t<T, kEncHwE2M2>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales, status,
                                                     row_skip, st);
         default:
             return launch_quantize_t<T, kEncGeneric>(w, rows, cols, rows_p, cols_p, e, m, maxrep, codes, scales,
@@ -860,6 +877,10 @@ static void launch_qpack(const void* w, uint32_t rows, uint32_t cols, uint32_t c
             break;
         case kEncHwE2M3:
             quantize_pack_kernel<T, kEncHwE2M3><<<grid, 32 * kPackWarps, 0, st>>>(wt, rows, cols, cols_p, ntiles, e, m,
+                                                                                 maxrep, scales, row_skip, bits, sd);
+            break;
+        case kEncHwE2M2:
+            quantize_pack_kernel<T, kEncHwE2M2><<<grid, 32 * kPackWarps, 0, st>>>(wt, rows, cols, cols_p, ntiles, e, m,
                                                                                  maxrep, scales, row_skip, bits, sd);
             break;
         default:

@@ -142,14 +142,20 @@ FPX_DEV void codes_low6_raw(uint32_t pa, uint32_t pb, uint32_t pc, int h, uint32
         c[3] = lop3_sel<0x30303030u>(pa << 4, pc);
     } else {
         // e2m2 [4,1] -> e2m3 code (c << 1): 4-bit group j%2 (S E1 E0 M1) -> bits 5:2,
-        // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0.
+        // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0.  The 1-bit
+        // word is split once into its odd / even bit positions, so that the
+        // neighbour shifted into bit 0 is already zero and one select LOP3
+        // per code word merges both (bits 7:6 are ignored by the conversion,
+        // as on the [2,4] path).
+        const uint32_t pe = pc & 0xaaaaaaaau, po = pc & 0x55555555u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t w4 = j < 2 ? pa : pb;
             const uint32_t hi = (j & 1) ? (w4 << 2) : shr<2>(w4);
             const int g = 4 * h + j;
-            const uint32_t lo = (g <= 6) ? (pc >> (6 - g)) : (pc << 1);
-            c[j] = (hi & 0x3c3c3c3cu) | (lo & 0x02020202u);
+            const uint32_t p1 = (g & 1) ? po : pe;
+            const uint32_t lo = (g <= 6) ? (p1 >> (6 - g)) : (p1 << 1);
+            c[j] = lop3_sel<0x3c3c3c3cu>(hi, lo);
         }
     }
 }

@@ -67,12 +67,13 @@ struct PArgs {
     const uint8_t* lo;
     int kt, tile_rows, split, ks, stages;
     unsigned long long* sink;
+    int hb = 1024, lb = 2048;  // stream bytes per 64x64 tile (e3m2: 2-bit hi, 4-bit lo)
 };
 __global__ void __launch_bounds__(64) pattern_read(PArgs a) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t full[32], empty[32];
     const uint32_t warp = threadIdx.x >> 5;
-    const int stage_bytes = 6 * 1024 * a.ks;
+    const int stage_bytes = 2 * (a.hb + a.lb) * a.ks;
     if (threadIdx.x == 0) {
         for (int i = 0; i < a.stages; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 1);
         fence_mbar_init();
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(64) pattern_read(PArgs a) {
                     uint8_t* d = sm + (size_t)s * stage_bytes;
                     for (int r = 0; r < 2; ++r) {
                         const size_t t = (size_t)(2 * mt + r) * a.kt + k;
-                        bulk_g2s(d + r * 1024 * a.ks, a.hi + t * 1024, 1024 * a.ks, &full[s], pol);
-                        bulk_g2s(d + 2048 * a.ks + r * 2048 * a.ks, a.lo + t * 2048, 2048 * a.ks, &full[s], pol);
+                        bulk_g2s(d + r * a.hb * a.ks, a.hi + t * a.hb, a.hb * a.ks, &full[s], pol);
+                        bulk_g2s(d + 2 * a.hb * a.ks + r * a.lb * a.ks, a.lo + t * a.lb, a.lb * a.ks, &full[s], pol);
                     }
                 }
             }
@@ -235,6 +236,28 @@ int main() {
             const double us = time_it(l, 12);
             printf("pattern grid %3d split %2d KS %d stages %2d (%3d KB ring): 135 MB b2b %5.1f us = %6.0f GB/s\n", c.grid,
                    c.split, c.ks, c.stages, smem / 1024, us, (hi_b + lo_b) / us / 1e3);
+            CK(cudaGetLastError());
+        }
+    }
+    // the same for e2m2 (4-bit hi 2 KB/tile, 1-bit lo 512 B/tile: 112.7 MB)
+    {
+        const int kt = 344, trs = 128;
+        const size_t hi_b = (size_t)trs * kt * 2048, lo_b = (size_t)trs * kt * 512;
+        uint8_t* pbuf;
+        CK(cudaMalloc(&pbuf, 3 * (hi_b + lo_b)));
+        CK(cudaMemset(pbuf, 1, 3 * (hi_b + lo_b)));
+        struct PC { int grid, split, ks, stages; };
+        for (PC c : {PC{128, 2, 2, 13}, PC{128, 2, 2, 16}, PC{128, 2, 4, 8}, PC{148, 9, 2, 13}}) {
+            const int smem = c.stages * 5 * 1024 * c.ks;
+            if (cudaFuncSetAttribute(pattern_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) continue;
+            auto l = [&](int r) {
+                const uint8_t* base = pbuf + (r % 3) * (hi_b + lo_b);
+                PArgs a{base, base + hi_b, kt, trs, c.split, c.ks, c.stages, sink, 2048, 512};
+                pattern_read<<<c.grid, 64, smem>>>(a);
+            };
+            const double us = time_it(l, 12);
+            printf("e2m2 pattern grid %3d split %2d KS %d stages %2d (%3d KB ring): %.1f MB b2b %5.1f us = %6.0f GB/s\n", c.grid,
+                   c.split, c.ks, c.stages, smem / 1024, (hi_b + lo_b) / 1e6, us, (hi_b + lo_b) / us / 1e3);
             CK(cudaGetLastError());
         }
     }
