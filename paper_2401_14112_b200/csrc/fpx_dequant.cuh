@@ -142,21 +142,26 @@ FPX_DEV void codes_low6_raw(uint32_t pa, uint32_t pb, uint32_t pc, int h, uint32
         c[3] = lop3_sel<0x30303030u>(pa << 4, pc);
     } else {
         // e2m2 [4,1] -> e2m3 code (c << 1): 4-bit group j%2 (S E1 E0 M1) -> bits 5:2,
-        // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0.  The 1-bit
-        // word is split once into its odd / even bit positions, so that the
-        // neighbour shifted into bit 0 is already zero and one select LOP3
-        // per code word merges both (bits 7:6 are ignored by the conversion,
-        // as on the [2,4] path).
-        const uint32_t pe = pc & 0xaaaaaaaau, po = pc & 0x55555555u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t w4 = j < 2 ? pa : pb;
-            const uint32_t hi = (j & 1) ? (w4 << 2) : shr<2>(w4);
-            const int g = 4 * h + j;
-            const uint32_t p1 = (g & 1) ? po : pe;
-            const uint32_t lo = (g <= 6) ? (p1 >> (6 - g)) : (p1 << 1);
-            c[j] = lop3_sel<0x3c3c3c3cu>(hi, lo);
-        }
+        // 1-bit group g = 4h+j (bit 7-g, M0) -> bit 1, bit 0 = 0 (bits 7:6
+        // are ignored by the conversion, as on the [2,4] path).
+        // * The half h's four 1-bit groups are brought to bits 7:4 of every
+        //   byte (x 16 for h = 1, an IMAD; bits 3:0 then hold the byte
+        //   below's groups and are never selected).
+        // * They are split into even / odd bit positions, so that whatever
+        //   lands next to a selected bit is zero, and each split is shifted
+        //   once for two code words: x (bits 7, 5 -> 3, 1) and y (bits 6, 4
+        //   -> 1 and bit 7 of the byte below; a rotate, so byte 0 gets byte
+        //   3's).
+        // * One select LOP3 per code word, plus one shift for words 0 and 3,
+        //   whose nibble and 1-bit group are merged before moving together.
+        const uint32_t pch = pc * (h ? 16u : 1u);
+        const uint32_t x = (pch & 0xaaaaaaaau) >> 4;
+        const uint32_t y = __funnelshift_r(pch & 0x55555555u, pch & 0x55555555u, 5);
+        c[0] = shr<2>(lop3_sel<0xf0f0f0f0u>(pa, x));
+        c[1] = lop3_sel<0x3c3c3c3cu>(pa << 2, y);
+        c[2] = lop3_sel<0x3c3c3c3cu>(shr<2>(pb), x);
+        const uint32_t t3 = lop3_sel<0x0f0f0f0fu>(pb, y);
+        c[3] = __funnelshift_l(t3, t3, 2);
     }
 }
 
