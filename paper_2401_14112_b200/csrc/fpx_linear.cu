@@ -1136,6 +1136,18 @@ cudaError_t launch_g(const LinearLaunch& L, const KParams& kp, int grid, cudaStr
 // NPAD=128 runs 3 groups, 4 measured equal).  N > 128: the single-issuer
 // kernel in 256-column chunks.  Tuning override (instantiated subset only):
 // FPX_LINEAR_CFG="KS,G" at NPAD 16 / 32.
+#ifndef FPX_N64_KS
+#define FPX_N64_KS 2
+#endif
+#ifndef FPX_N64_G
+#define FPX_N64_G 4
+#endif
+#ifndef FPX_N128_KS
+#define FPX_N128_KS 2
+#endif
+#ifndef FPX_N128_G
+#define FPX_N128_G 3
+#endif
 template <int F>
 cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, int grid, cudaStream_t st) {
     int ks = 0, ng = 0;
@@ -1155,8 +1167,8 @@ cudaError_t launch_f(const LinearLaunch& L, const KParams& kp, uint32_t npad, in
         if (ks == 2 && ng == 3) return launch_g<F, 32, 2, 3>(L, kp, grid, st);
         return launch_g<F, 32, 2, 4>(L, kp, grid, st);
     }
-    if (npad == 64) return launch_g<F, 64, 2, 4>(L, kp, grid, st);
-    if (npad == 128) return launch_g<F, 128, 2, 3>(L, kp, grid, st);
+    if (npad == 64) return launch_g<F, 64, FPX_N64_KS, FPX_N64_G>(L, kp, grid, st);
+    if (npad == 128) return launch_g<F, 128, FPX_N128_KS, FPX_N128_G>(L, kp, grid, st);
     if (npad == 256) return launch_t<F, 256, 1, 2>(L, kp, grid, st);
     return cudaErrorInvalidValue;
 }
