@@ -68,6 +68,8 @@ struct PArgs {
     int kt, tile_rows, split, ks, stages;
     unsigned long long* sink;
     int hb = 1024, lb = 2048;  // stream bytes per 64x64 tile (e3m2: 2-bit hi, 4-bit lo)
+    int passes = 1;            // linears streamed back to back inside ONE launch
+    size_t pass_stride = 0;    // bytes between the passes' weight copies (3 rotated)
 };
 __global__ void __launch_bounds__(64) pattern_read(PArgs a) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -85,7 +87,9 @@ __global__ void __launch_bounds__(64) pattern_read(PArgs a) {
     if (warp == 0) {
         if (elect_one()) {
             uint32_t i = 0;
+            for (int pass = 0; pass < a.passes; ++pass)
             for (int u = u0; u < u1; ++u) {
+                const size_t po = (pass % 3) * a.pass_stride;
                 const int mt = u / a.split, ch = u % a.split;
                 const int k0 = ch * a.kt / a.split, k1 = (ch + 1) * a.kt / a.split;
                 for (int k = k0; k + a.ks <= k1; k += a.ks, ++i) {
@@ -95,14 +99,16 @@ __global__ void __launch_bounds__(64) pattern_read(PArgs a) {
                     uint8_t* d = sm + (size_t)s * stage_bytes;
                     for (int r = 0; r < 2; ++r) {
                         const size_t t = (size_t)(2 * mt + r) * a.kt + k;
-                        bulk_g2s(d + r * a.hb * a.ks, a.hi + t * a.hb, a.hb * a.ks, &full[s], pol);
-                        bulk_g2s(d + 2 * a.hb * a.ks + r * a.lb * a.ks, a.lo + t * a.lb, a.lb * a.ks, &full[s], pol);
+                        bulk_g2s(d + r * a.hb * a.ks, a.hi + po + t * a.hb, a.hb * a.ks, &full[s], pol);
+                        bulk_g2s(d + 2 * a.hb * a.ks + r * a.lb * a.ks, a.lo + po + t * a.lb, a.lb * a.ks, &full[s],
+                                 pol);
                     }
                 }
             }
         }
     } else {
         uint32_t i = 0, acc = 0;
+        for (int pass = 0; pass < a.passes; ++pass)
         for (int u = u0; u < u1; ++u) {
             const int ch = u % a.split;
             const int k0 = ch * a.kt / a.split, k1 = (ch + 1) * a.kt / a.split;
@@ -238,6 +244,32 @@ int main() {
                    c.split, c.ks, c.stages, smem / 1024, us, (hi_b + lo_b) / us / 1e3);
             CK(cudaGetLastError());
         }
+    }
+    // launch boundaries: the e3m2 pattern, 6 linears per launch vs 1
+    {
+        const int kt = 344, trs = 128;
+        const size_t hi_b = (size_t)trs * kt * 1024, lo_b = (size_t)trs * kt * 2048;
+        uint8_t* pbuf;
+        CK(cudaMalloc(&pbuf, 3 * (hi_b + lo_b)));
+        CK(cudaMemset(pbuf, 1, 3 * (hi_b + lo_b)));
+        for (int grid : {128, 148}) {
+            const int split = grid == 128 ? 2 : 37, stages = 13, smem = stages * 6 * 1024 * 2;
+            cudaFuncSetAttribute(pattern_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            for (int passes : {1, 6}) {
+                auto l = [&](int r) {
+                    const uint8_t* base = pbuf + (passes == 1 ? (r % 3) * (hi_b + lo_b) : 0);
+                    PArgs a{base, base + hi_b, kt, trs, split, 2, stages, sink};
+                    a.passes = passes;
+                    a.pass_stride = hi_b + lo_b;
+                    pattern_read<<<grid, 64, smem>>>(a);
+                };
+                const double us = time_it(l, 12) / passes;
+                printf("boundary grid %3d split %2d: %d linear(s) per launch: %5.1f us per 135 MB linear = %6.0f GB/s\n",
+                       grid, split, passes, us, (hi_b + lo_b) / us / 1e3);
+                CK(cudaGetLastError());
+            }
+        }
+        cudaFree(pbuf);
     }
     // the same for e2m2 (4-bit hi 2 KB/tile, 1-bit lo 512 B/tile: 112.7 MB)
     {
