@@ -87,6 +87,12 @@ __device__ __forceinline__ uint32_t cvt_fp6x2(float lo, float hi) {
     return r;
 }
 
+__device__ __noinline__ uint32_t encode4_exact_slow(float4 v, float sv, float inv, int e, int m, int bias,
+                                                    uint32_t cmax) {
+    return encode_exact(v.x, sv, inv, e, m, bias, cmax) | encode_exact(v.y, sv, inv, e, m, bias, cmax) << 8 |
+           encode_exact(v.z, sv, inv, e, m, bias, cmax) << 16 | encode_exact(v.w, sv, inv, e, m, bias, cmax) << 24;
+}
+
 template <int MODE>
 __device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e, int m, int bias, uint32_t cmax) {
     if constexpr (MODE == kEncGeneric) {
@@ -99,8 +105,8 @@ __device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e
         constexpr float kUp = 1.0f + 0x1p-20f, kDn = 1.0f - 0x1p-20f;
         const uint32_t up = cvt_fp6x2<MODE>(qa * kUp, qb * kUp) | cvt_fp6x2<MODE>(qc * kUp, qd * kUp) << 16;
         const uint32_t dn = cvt_fp6x2<MODE>(qa * kDn, qb * kDn) | cvt_fp6x2<MODE>(qc * kDn, qd * kDn) << 16;
-        if (up != dn)  // a quotient near a rounding boundary
-            return encode4<kEncGeneric>(v, sv, inv, e, m, bias, cmax);
+        if (up != dn)  // a quotient near a rounding boundary (rare: kept out of line)
+            return encode4_exact_slow(v, sv, inv, e, m, bias, cmax);
         const uint32_t sgn = ((__float_as_uint(v.x) >> 31) | (__float_as_uint(v.y) >> 31) << 8 |
                               (__float_as_uint(v.z) >> 31) << 16 | (__float_as_uint(v.w) >> 31) << 24)
                              << (k5 ? 4 : 5);
@@ -148,6 +154,38 @@ __device__ __forceinline__ void load_w16(const float* p, float4 (&v)[1]) {
 }
 __device__ __forceinline__ void load_w16(const uint16_t* p, float4 (&v)[2]) {
     const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+    const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+    v[0] = make_float4(a.x, a.y, b.x, b.y);
+    v[1] = make_float4(c.x, c.y, d.x, d.y);
+}
+
+// The 16 bytes of a row at column c when they run past `cols` (or are not
+// 16-byte aligned): element-wise, +0.0 past the end.
+__device__ __forceinline__ uint4 load_raw16_ragged(const float* row, uint32_t c, uint32_t cols) {
+    uint32_t x[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) x[q] = c + q < cols ? __float_as_uint(row[c + q]) : 0u;
+    return make_uint4(x[0], x[1], x[2], x[3]);
+}
+__device__ __forceinline__ uint4 load_raw16_ragged(const uint16_t* row, uint32_t c, uint32_t cols) {
+    uint32_t x[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t a = c + 2 * q < cols ? row[c + 2 * q] : 0u;
+        const uint32_t b = c + 2 * q + 1 < cols ? row[c + 2 * q + 1] : 0u;
+        x[q] = a | (b << 16);
+    }
+    return make_uint4(x[0], x[1], x[2], x[3]);
+}
+
+// 16 raw bytes of a row as groups of 4 weights (exact widening).
+__device__ __forceinline__ void raw16_to_float4(const uint4& u, float4 (&v)[1]) {
+    v[0] = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
+__device__ __forceinline__ void raw16_to_float4(const uint4& u, float4 (&v)[2]) {
     const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
     const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
     const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
@@ -462,24 +500,25 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
     (void)maxrep;
     // Each lane reads 16 bytes of one row per pass -- kG groups of 4 weights
     // (fp32: 1, fp16: 2) -- so kLpr lanes cover a 64-weight tile row and a
-    // pass covers kRpp rows; passes run in chunks with every load of the
-    // chunk issued first (loads depend only on indices; row scales and skip
-    // flags load alongside and apply after).
+    // pass covers kRpp rows.  Passes run in chunks of kChunk with every load
+    // of the chunk issued first, kept as raw 16-byte words (converted to fp32
+    // only at the encode), so both dtypes keep 128 bytes per lane in flight;
+    // row scales and skip flags load alongside and apply after.
     constexpr uint32_t kG = 16u / (4u * sizeof(T)), kLpr = 16u / kG, kRpp = 32u / kLpr;
-    constexpr uint32_t kChunk = 8u / kG;
+    constexpr uint32_t kChunk = 8u;
+    static_assert((64u / kRpp) % kChunk == 0, "passes per chunk");
     const uint32_t cc = (t % kLpr) * 4u * kG, c = c0 + cc;
     const bool full = c + 4u * kG <= cols;
     const bool vec = (reinterpret_cast<uintptr_t>(w) % 16u) == 0 && (static_cast<size_t>(cols) * sizeof(T)) % 16u == 0;
 #pragma unroll 1
     for (uint32_t i0 = 0; i0 < 64u / kRpp; i0 += kChunk) {
-        float4 v[kChunk][kG];
+        uint4 raw[kChunk];
         uint16_t sraw[kChunk];
         uint8_t skip[kChunk];
 #pragma unroll
         for (uint32_t j = 0; j < kChunk; ++j) {
             const uint32_t r = r0 + kRpp * (i0 + j) + t / kLpr;
-#pragma unroll
-            for (uint32_t gq = 0; gq < kG; ++gq) v[j][gq] = make_float4(0.f, 0.f, 0.f, 0.f);
+            raw[j] = make_uint4(0u, 0u, 0u, 0u);  // +0.0 in either dtype: code 0
             sraw[j] = 0x3c00u;
             skip[j] = 1;
             if (r < rows) {
@@ -487,14 +526,9 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
                 sraw[j] = scales[r];
                 skip[j] = row_skip[r];
                 if (full && vec) {
-                    load_w16(row + c, v[j]);
+                    raw[j] = __ldcs(reinterpret_cast<const uint4*>(row + c));
                 } else {
-#pragma unroll
-                    for (uint32_t q = 0; q < 4u * kG; ++q) {
-                        const float x = c + q < cols ? load_w(row + c + q) : 0.0f;
-                        float* f = reinterpret_cast<float*>(&v[j][q / 4]);
-                        f[q % 4] = x;
-                    }
+                    raw[j] = load_raw16_ragged(row, c, cols);
                 }
             }
         }
@@ -506,9 +540,11 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
             for (uint32_t gq = 0; gq < kG; ++gq) packed[gq] = 0u;
             if (!skip[j]) {
                 const float sv = __half2float(__ushort_as_half(sraw[j])), inv = __frcp_rn(sv);
+                float4 v[kG];
+                raw16_to_float4(raw[j], v);
 #pragma unroll
                 for (uint32_t gq = 0; gq < kG; ++gq)  // columns >= cols hold +0.0: code 0
-                    packed[gq] = encode4<MODE>(v[j][gq], sv, inv, e, m, bias, cmax);
+                    packed[gq] = encode4<MODE>(v[gq], sv, inv, e, m, bias, cmax);
             }
             if constexpr (kG == 1)
                 *reinterpret_cast<uint32_t*>(ts + rr * kTileStride + cc) = packed[0];
