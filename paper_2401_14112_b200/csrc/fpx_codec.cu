@@ -194,6 +194,42 @@ __device__ __forceinline__ void raw16_to_float4(const uint4& u, float4 (&v)[2]) 
     v[1] = make_float4(c.x, c.y, d.x, d.y);
 }
 
+// Thread 0 of a row's CTA, after the row max: fp16 scale via
+// double -> float -> half (codec.cpp:145), zero-scale bump (:153), effective
+// scale check (:155-164); failures folded into the status key (:173-174).
+__device__ __forceinline__ void decide_row_scale(uint32_t r, float a, bool nan, int e, double maxrep,
+                                                 uint16_t* scales, unsigned long long* status, uint8_t* row_skip,
+                                                 int& skip, float& s_val) {
+    int st = 0;
+    uint16_t s16 = 0x3c00u;
+    skip = 0;
+    if (nan) {
+        st = 3;  // InvalidValue
+    } else if (a == 0.0f) {
+        skip = 1;  // all-zero row: scale 1.0, codes 0
+    } else {
+        const double q = static_cast<double>(a) / maxrep;
+        s16 = __half_as_ushort(__float2half_rn(__double2float_rn(q)));
+        if ((s16 & 0x7c00u) == 0x7c00u) {
+            st = 4;  // ScaleOverflow
+        } else {
+            if ((s16 & 0x7fffu) == 0u) s16 = static_cast<uint16_t>((s16 & 0x8000u) | 1u);
+            const double sv = static_cast<double>(__half2float(__ushort_as_half(s16)));
+            const double ev = sv * ldexp(1.0, 15 - ((1 << (e - 1)) - 1));
+            const uint16_t eff = __half_as_ushort(__float2half_rn(__double2float_rn(ev)));
+            if ((eff & 0x7c00u) == 0x7c00u) st = 4;
+        }
+    }
+    if (st) {
+        atomicMin(status, (static_cast<unsigned long long>(r) << 8) | static_cast<unsigned>(st));
+        skip = 1;
+        s16 = 0x3c00u;
+    }
+    scales[r] = s16;
+    if (row_skip) row_skip[r] = static_cast<uint8_t>(skip);
+    s_val = __half2float(__ushort_as_half(s16));
+}
+
 // Row pass: scale + status (+ the row's codes when codes != nullptr).
 // codes == nullptr: row scales, status and the per-row skip flag only (pass 1
 // of the fused quantize+pack, whose tile kernel encodes and packs).
@@ -287,34 +323,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
     if (threadIdx.x == 0) {
         float a = 0.0f;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a = fmaxf(a, red[i]);
-        int st = 0;
-        uint16_t s16 = 0x3c00u;
-        skip = 0;
-        if (nan_flag) {
-            st = 3;  // InvalidValue
-        } else if (a == 0.0f) {
-            skip = 1;  // all-zero row: scale 1.0, codes 0
-        } else {
-            const double q = static_cast<double>(a) / maxrep;
-            s16 = __half_as_ushort(__float2half_rn(__double2float_rn(q)));
-            if ((s16 & 0x7c00u) == 0x7c00u) {
-                st = 4;  // ScaleOverflow
-            } else {
-                if ((s16 & 0x7fffu) == 0u) s16 = static_cast<uint16_t>((s16 & 0x8000u) | 1u);
-                const double sv = static_cast<double>(__half2float(__ushort_as_half(s16)));
-                const double ev = sv * ldexp(1.0, 15 - ((1 << (e - 1)) - 1));
-                const uint16_t eff = __half_as_ushort(__float2half_rn(__double2float_rn(ev)));
-                if ((eff & 0x7c00u) == 0x7c00u) st = 4;
-            }
-        }
-        if (st) {
-            atomicMin(status, (static_cast<unsigned long long>(r) << 8) | static_cast<unsigned>(st));
-            skip = 1;
-            s16 = 0x3c00u;
-        }
-        scales[r] = s16;
-        if (row_skip) row_skip[r] = static_cast<uint8_t>(skip);
-        s_val = __half2float(__ushort_as_half(s16));
+        decide_row_scale(r, a, nan_flag != 0, e, maxrep, scales, status, row_skip, skip, s_val);
     }
     if (codes == nullptr) return;
     __syncthreads();
@@ -357,6 +366,90 @@ __global__ void __launch_bounds__(256) quantize_kernel(const T* __restrict__ w, 
         }
         *reinterpret_cast<uint32_t*>(out + c) = packed;
     }
+}
+
+// K0 with the row staged in shared memory (rows of at most kStageMax
+// bytes, 16-byte aligned): one bulk copy brings the whole row in -- up to
+// ~88 KB in flight per CTA with no per-thread load slots -- and both the max
+// and the encode read it from shared memory, so HBM sees each weight once
+// (the two-pass kernel above re-reads most rows from DRAM: ~1.3 GB of reads
+// for 0.72 GB of fp32 weights at 8192 x 22016).
+cudaError_t ensure_smem_attr(const void* kern, int bytes);  // fpx_linear.cu (per device)
+constexpr uint32_t kStageMax = 200u * 1024u;
+constexpr uint32_t kStageChunk = 32u * 1024u;
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) quantize_staged_kernel(const T* __restrict__ w, uint32_t cols, uint32_t cols_p,
+                                                              int e, int m, double maxrep, uint8_t* __restrict__ codes,
+                                                              uint16_t* __restrict__ scales,
+                                                              unsigned long long* __restrict__ status) {
+    extern __shared__ __align__(16) uint8_t srow[];
+    __shared__ uint64_t full;
+    __shared__ float red[8];
+    __shared__ int nan_flag;
+    __shared__ float s_val;
+    __shared__ int skip;
+    const uint32_t r = blockIdx.x;
+    const uint32_t bytes = cols * sizeof(T);  // % 16 == 0 (host check)
+    if (threadIdx.x == 0) {
+        nan_flag = 0;
+        mbar_init(&full, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&full, bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(w + static_cast<size_t>(r) * cols);
+        const uint64_t pol = policy_evict_first();
+        for (uint32_t o = 0; o < bytes; o += kStageChunk)
+            bulk_g2s(srow + o, src + o, min(kStageChunk, bytes - o), &full, pol);
+    }
+    __syncthreads();
+    mbar_wait(&full, 0);
+    constexpr uint32_t kG = 16u / (4u * sizeof(T));  // groups of 4 weights per 16 bytes
+    const uint32_t n16 = bytes / 16u;
+    float amax = 0.0f;
+    bool nan = false;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+        float4 v[kG];
+        raw16_to_float4(reinterpret_cast<const uint4*>(srow)[i], v);
+#pragma unroll
+        for (uint32_t gq = 0; gq < kG; ++gq) {
+            const float4 x = v[gq];
+            nan |= isnan(x.x) | isnan(x.y) | isnan(x.z) | isnan(x.w);
+            amax = fmaxf(fmaxf(amax, fmaxf(fabsf(x.x), fabsf(x.y))), fmaxf(fabsf(x.z), fabsf(x.w)));
+        }
+    }
+    if (nan) nan_flag = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float a = 0.0f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a = fmaxf(a, red[i]);
+        decide_row_scale(r, a, nan_flag != 0, e, maxrep, scales, status, nullptr, skip, s_val);
+    }
+    __syncthreads();
+    const int bias = (1 << (e - 1)) - 1;
+    const float sv = s_val, inv = __frcp_rn(s_val);
+    const uint32_t cmax = (1u << (e + m)) - 1u;
+    uint8_t* out = codes + static_cast<size_t>(r) * cols_p;
+    // 16 bytes of weights -> kG code words; columns past cols (to cols_p) get code 0
+    if (skip) {
+        for (uint32_t c = threadIdx.x * 4; c < cols_p; c += blockDim.x * 4) *reinterpret_cast<uint32_t*>(out + c) = 0u;
+        return;
+    }
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+        float4 v[kG];
+        raw16_to_float4(reinterpret_cast<const uint4*>(srow)[i], v);
+        uint32_t packed[kG];
+#pragma unroll
+        for (uint32_t gq = 0; gq < kG; ++gq) packed[gq] = encode4<MODE>(v[gq], sv, inv, e, m, bias, cmax);
+        if constexpr (kG == 1)
+            *reinterpret_cast<uint32_t*>(out + 4 * i) = packed[0];
+        else
+            *reinterpret_cast<uint2*>(out + 8 * i) = make_uint2(packed[0], packed[kG - 1]);
+    }
+    for (uint32_t c = cols + threadIdx.x * 4; c < cols_p; c += blockDim.x * 4)
+        *reinterpret_cast<uint32_t*>(out + c) = 0u;
 }
 
 // ------------------------------------------------------------------ K1
@@ -865,6 +958,24 @@ template <typename T, int MODE>
 static void launch_quantize_t(const void* w, uint32_t rows, uint32_t cols, uint32_t rows_p, uint32_t cols_p, int e,
                               int m, double maxrep, uint8_t* codes, uint16_t* scales, unsigned long long* status,
                               uint8_t* row_skip, cudaStream_t st) {
+    const size_t bytes = static_cast<size_t>(cols) * sizeof(T);
+    // whole rows in shared memory when they fit and are 16-byte aligned (the
+    // padding rows past `rows` stay with the two-pass kernel below)
+    if (codes != nullptr && row_skip == nullptr && bytes % 16 == 0 && bytes <= kStageMax &&
+        reinterpret_cast<uintptr_t>(w) % 16 == 0 && cols % 4 == 0) {
+        auto kern = quantize_staged_kernel<T, MODE>;
+        if (ensure_smem_attr(reinterpret_cast<const void*>(kern), static_cast<int>(kStageMax)) == cudaSuccess) {
+            kern<<<rows, 256, bytes, st>>>(static_cast<const T*>(w), cols, cols_p, e, m, maxrep, codes, scales,
+                                           status);
+            if (rows_p > rows)  // padding rows: codes 0, scale 1.0
+                quantize_kernel<T, MODE><<<rows_p - rows, 256, 0, st>>>(static_cast<const T*>(w), 0, cols, cols_p, e,
+                                                                        m, maxrep, codes + static_cast<size_t>(rows) *
+                                                                                               cols_p,
+                                                                        scales + rows, status, row_skip);
+            return;
+        }
+        (void)cudaGetLastError();
+    }
     quantize_kernel<T, MODE><<<rows_p, 256, 0, st>>>(static_cast<const T*>(w), rows, cols, cols_p, e, m, maxrep, codes,
                                                      scales, status, row_skip);
 }
