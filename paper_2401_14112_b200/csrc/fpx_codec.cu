@@ -722,7 +722,10 @@ __global__ void __launch_bounds__(64) dequant_reg_kernel(const uint8_t* __restri
                                                           const uint8_t* __restrict__ s_lo,
                                                           const uint16_t* __restrict__ scales,
                                                           uint32_t cols_p, uint16_t* __restrict__ out) {
-    __shared__ __align__(16) uint16_t tile_s[64 * 64];
+    // row stride 72 halves (144 B): the 8 rows one fragment store touches
+    // land 4 banks apart (64 would put them all on the same 4 banks)
+    constexpr uint32_t kStr = 72u;
+    __shared__ __align__(16) uint16_t tile_s[64 * kStr];
     constexpr int kHi = FmtTraits<F>::kBitsHi, kLo = FmtTraits<F>::kBitsLo;
     const uint32_t tile = blockIdx.x;
     const uint32_t h = threadIdx.x >> 5, t = threadIdx.x & 31u;
@@ -753,16 +756,16 @@ __global__ void __launch_bounds__(64) dequant_reg_kernel(const uint8_t* __restri
             const uint32_t k0 = 32u * s + 4u * (4u * h + j);
             uint32_t rr, cc;
             code_rc(t, k0, rr, cc);  // pair of (k0, k0+1): same row, cols cc, cc+1
-            *reinterpret_cast<uint32_t*>(&tile_s[rr * 64u + cc]) = r1[j];
+            *reinterpret_cast<uint32_t*>(&tile_s[rr * kStr + cc]) = r1[j];
             code_rc(t, k0 + 2u, rr, cc);
-            *reinterpret_cast<uint32_t*>(&tile_s[rr * 64u + cc]) = r2[j];
+            *reinterpret_cast<uint32_t*>(&tile_s[rr * kStr + cc]) = r2[j];
         }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < 64u * 8u; i += 64u) {  // 64 rows x 8 uint4
         const uint32_t rr = i >> 3, cc = (i & 7u) * 8u;
         *reinterpret_cast<uint4*>(out + static_cast<size_t>(tr * 64u + rr) * cols_p + tc * 64u + cc) =
-            *reinterpret_cast<const uint4*>(&tile_s[rr * 64u + cc]);
+            *reinterpret_cast<const uint4*>(&tile_s[rr * kStr + cc]);
     }
 }
 
