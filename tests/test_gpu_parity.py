@@ -865,3 +865,35 @@ def test_sharded_linear_multiprocess_c_abi_chain(cuda, world):
         assert pr.exitcode == 0
     for rank, oks in res:
         assert all(oks), f"rank {rank}: sharded C differs from the 1-GPU launch: {oks}"
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("e,m", [(3, 2), (2, 2)])
+def test_quantize_staged_and_two_pass_rows(cuda, oracle, dtype, e, m):
+    """K0 stages 16-byte aligned rows of at most 200 KB in shared memory
+    (quantize_staged_kernel) and runs the two-pass row kernel otherwise:
+    shapes on both sides of each condition -- row bytes % 16, the 200 KB
+    limit exactly, padding rows and columns -- with a NaN row and an
+    all-zero row, codes and scales bit for bit against the oracle."""
+    fpx = _fpx()
+    esz = 4 if dtype == "fp32" else 2
+    rng = np.random.default_rng(7 * e + m + esz)
+    limit = 200 * 1024 // esz
+    shapes = [(70, 96), (70, 100), (66, 98), (5, 104), (2, limit), (2, limit + 64), (1, 40)]
+    for rows, cols in shapes:
+        w = (rng.standard_normal((rows, cols)) * 0.05).astype(np.float32)
+        w[rows // 2, :] = 0.0
+        if dtype == "fp16":
+            w = w.astype(np.float16).astype(np.float32)  # the oracle sees the exact fp16 values
+        st, codes, scales, _ = oracle.quantize(w, e, m)
+        assert st == 0
+        t = torch.from_numpy(w).to(cuda)
+        q = fpx.quantize_matrix(t if dtype == "fp32" else t.half(), fpx.FpxFormat(e, m))
+        assert (q.codes.cpu().numpy() == codes).all(), (rows, cols)
+        assert (q.scales.cpu().numpy().view(np.uint16) == scales).all(), (rows, cols)
+        if rows > 2:
+            w[rows - 1, cols // 3] = float("nan")
+            t = torch.from_numpy(w).to(cuda)
+            with pytest.raises(fpx.FpxError) as ei:
+                fpx.quantize_matrix(t if dtype == "fp32" else t.half(), fpx.FpxFormat(e, m))
+            assert ei.value.code == fpx.ErrorCode.InvalidValue and f"row {rows - 1}" in str(ei.value)
