@@ -234,6 +234,18 @@ def make_packed(ctx, rows, cols, seed, fmt=(3, 2)):
     return p
 
 
+def page_locked(torch, t):
+    """Pin a CPU tensor in place with cudaHostRegister.  Copies from it run
+    at the PCIe rate (~52 GB/s H2D on B200 boxes), while H2D copies from
+    torch's own pinned-memory allocator measured 12-25 GB/s on some boxes
+    (tools/pinned_probe.py).  The registration lives as long as the process."""
+    t = t.contiguous()
+    err = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), t.numel() * t.element_size(), 0)
+    if int(err) != 0:
+        return t.pin_memory()
+    return t
+
+
 def clone_packed(ctx, p):
     return ctx.fpx.PackedWeights(p.format, p.split, p.rows, p.cols, p.orig_rows, p.orig_cols,
                                  [s.clone() for s in p.streams], p.scales.clone())
@@ -360,6 +372,9 @@ STACK70B = (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate", 28672, 8192), ("up
             ("down", 8192, 28672))
 
 
+STACK70B_MERGED = (("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672))
+
+
 def measure_stack70b(ctx, batches, layers=80):
     """BASELINE configs[4]: the LLaMA-70B decoder linear stack, 80 layers x
     (QKV, O, gate, up, down), FP6 e3m2, column-sharded over the ranks (rank r
@@ -367,59 +382,82 @@ def measure_stack70b(ctx, batches, layers=80):
     of packed weights).  One pass = the 400 linears in order, each on the batch
     and -- at world > 1 -- followed by the NCCL all-gather of its output
     (fpx_linear_sharded, shard-local split); at world 1 plain fpx_linear.
-    Timed as one CUDA graph per batch.  Weight GB/s counts the full stack."""
+    Timed as one CUDA graph per batch.  Weight GB/s counts the full stack.
+    `merged_gate_up`: the same stack with gate and up as ONE 57344-row linear
+    (PackedWeights.concat_rows layout: both read the same activations), 320
+    launches per pass -- the same weight bytes, one launch boundary less per
+    layer."""
     import ctypes as C
     torch, L, fpx = ctx.torch, ctx.L, ctx.fpx
-    import math
     from paper_2401_14112_b200 import shard
     t0 = time.time()
-    packs = []  # [layer][linear] -> (PackedWeights shard, ptr array)
-    for layer in range(layers):
-        row = []
-        for j, (_, M, K) in enumerate(STACK70B):
-            tr0, tr1 = shard.shard_tile_rows(M, ctx.rank, ctx.world)
-            p = make_packed(ctx, (tr1 - tr0) * 64, K, seed=7000 + 10 * layer + j + 100000 * ctx.rank)
-            row.append((p, (C.c_void_p * 2)(*[s.data_ptr() for s in p.streams])))
-        packs.append(row)
+
+    def build(spec, seed0):
+        packs = []  # [layer][linear] -> (PackedWeights shard, ptr array)
+        for layer in range(layers):
+            row = []
+            for j, (_, M, K) in enumerate(spec):
+                tr0, tr1 = shard.shard_tile_rows(M, ctx.rank, ctx.world)
+                p = make_packed(ctx, (tr1 - tr0) * 64, K, seed=seed0 + 10 * layer + j + 100000 * ctx.rank)
+                row.append((p, (C.c_void_p * 2)(*[s.data_ptr() for s in p.streams])))
+            packs.append(row)
+        return packs
+
+    packs = build(STACK70B, 7000)
     torch.cuda.synchronize(ctx.dev)
     setup_s = time.time() - t0
     full_bytes = layers * sum(M * K * 6 // 8 for _, M, K in STACK70B)
-    res = {}
     nmax = max(batches)
     acts = {K: torch.randn(nmax, K, device=ctx.dev).half() for K in (8192, 28672)}
-    outs = {M: torch.empty(nmax, M, device=ctx.dev) for _, M, _ in STACK70B}
+    outs = {M: torch.empty(nmax, M, device=ctx.dev) for M in {M for _, M, _ in STACK70B + STACK70B_MERGED}}
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device=ctx.dev)
-    for n in batches:
-        if ctx.world == 1:
-            def one(p, ptrs, M, K):
-                st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
-                                  outs[M].data_ptr(), M, 0, ws.data_ptr(), ws.numel(), ctx.stream())
-                assert st == 0, L.fpx_last_error()
-        else:
-            def one(p, ptrs, M, K):
-                st = L.fpx_linear_sharded(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
-                                          outs[M].data_ptr(), M, -1, ctx.rank, ctx.world, ctx.comm, ws.data_ptr(),
-                                          ws.numel(), ctx.stream())
-                assert st == 0, L.fpx_last_error()
 
-        def stack_pass():
-            for row in packs:
-                for (p, ptrs), (_, M, K) in zip(row, STACK70B):
-                    one(p, ptrs, M, K)
+    def time_stack(packs, spec):
+        res = {}
+        for n in batches:
+            if ctx.world == 1:
+                def one(p, ptrs, M, K):
+                    st = L.fpx_linear(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
+                                      outs[M].data_ptr(), M, 0, ws.data_ptr(), ws.numel(), ctx.stream())
+                    assert st == 0, L.fpx_last_error()
+            else:
+                def one(p, ptrs, M, K):
+                    st = L.fpx_linear_sharded(ptrs, 2, p.scales.data_ptr(), M, K, 3, 2, acts[K].data_ptr(), K, n,
+                                              outs[M].data_ptr(), M, -1, ctx.rank, ctx.world, ctx.comm,
+                                              ws.data_ptr(), ws.numel(), ctx.stream())
+                    assert st == 0, L.fpx_last_error()
 
-        stack_pass()
-        gr = ctx.capture(stack_pass)
-        ms = ctx.max_over_ranks(ctx.timed(gr, 2) / 2)
-        res[str(n)] = {"ms": round(ms, 3), "weight_GBps": round(full_bytes / (ms * 1e-3) / 1e9, 1),
-                       "TFLOPs": round(2.0 * full_bytes * 8 / 6 * n / (ms * 1e-3) / 1e12, 1)}
-        del gr
+            def stack_pass():
+                for row in packs:
+                    for (p, ptrs), (_, M, K) in zip(row, spec):
+                        one(p, ptrs, M, K)
+
+            stack_pass()
+            gr = ctx.capture(stack_pass)
+            ms = ctx.max_over_ranks(ctx.timed(gr, 2) / 2)
+            res[str(n)] = {"ms": round(ms, 3), "weight_GBps": round(full_bytes / (ms * 1e-3) / 1e9, 1),
+                           "TFLOPs": round(2.0 * full_bytes * 8 / 6 * n / (ms * 1e-3) / 1e12, 1)}
+            del gr
+        return res
+
+    res = time_stack(packs, STACK70B)
+    # merged variant: QKV / O / down reused, gate + up as one linear
+    merged_packs = []
+    for layer, row in enumerate(packs):
+        tr0, tr1 = shard.shard_tile_rows(57344, ctx.rank, ctx.world)
+        gu = make_packed(ctx, (tr1 - tr0) * 64, 8192, seed=9000 + layer + 100000 * ctx.rank)
+        merged_packs.append([row[0], row[1], (gu, (C.c_void_p * 2)(*[s.data_ptr() for s in gu.streams])), row[4]])
     del packs
+    torch.cuda.empty_cache()
+    res_m = time_stack(merged_packs, STACK70B_MERGED)
+    del merged_packs
     torch.cuda.empty_cache()
     return {"layers": layers, "linears": [f"{nm} {M}x{K}" for nm, M, K in STACK70B],
             "weight_bytes": full_bytes, "world": ctx.world,
             "sharding": "column (output rows) per rank + NCCL all-gather per linear" if ctx.world > 1 else "1 GPU",
             "setup_s": round(setup_s, 1), "per_batch": res,
-            "timing": "one CUDA graph of the 400 linears per batch, 2 replays, max over ranks"}
+            "merged_gate_up": {"linears": [f"{nm} {M}x{K}" for nm, M, K in STACK70B_MERGED], "per_batch": res_m},
+            "timing": "one CUDA graph of the 400 (merged: 320) linears per batch, 2 replays, max over ranks"}
 
 
 def run_ours(args, rank, world, local):
@@ -509,8 +547,8 @@ def run_ours(args, rank, world, local):
         # (each small cudaMemcpy costs several us of copy-engine time).
         tot_a = sum(n * K_COLS for n in batches)
         tot_c = sum(n * rows_out for n in batches)
-        h_act_all = torch.cat([acts[n].reshape(-1) for n in batches]).cpu().pin_memory()
-        h_out_all = torch.empty(tot_c, pin_memory=True)
+        h_act_all = page_locked(torch, torch.cat([acts[n].reshape(-1) for n in batches]).cpu())
+        h_out_all = page_locked(torch, torch.empty(tot_c))
 
         def views(buf, per_row):
             out, off = {}, 0

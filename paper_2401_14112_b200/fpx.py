@@ -180,6 +180,27 @@ class PackedWeights:
     def tile_stream_bytes(w: int) -> int:
         return 512 * w
 
+    @staticmethod
+    def concat_rows(parts: list) -> "PackedWeights":
+        """The inverse of shard(): several packed weights with the same format,
+        split and padded K stacked along the output rows into ONE packed
+        weight (a byte concatenation of every stream and of the scales, since
+        tiles are stored in row-major tile order).  Linears that read the same
+        activations -- gate and up of a LLaMA MLP, separate Q / K / V -- then
+        run as one launch.  Part i's rows start at the sum of the previous
+        parts' padded row counts; padding rows stay (code 0, zero output)."""
+        if not parts:
+            raise FpxError(3, "error[invalid-value] nothing to concatenate")
+        p0 = parts[0]
+        for p in parts[1:]:
+            if (p.format.exp_bits, p.format.man_bits) != (p0.format.exp_bits, p0.format.man_bits) or \
+                    p.split.widths != p0.split.widths or p.cols != p0.cols:
+                raise FpxError(5, "error[shape-mismatch] concat_rows needs one format, split and padded K")
+        streams = [torch.cat([p.streams[i].reshape(-1) for p in parts]) for i in range(len(p0.streams))]
+        rows = sum(p.rows for p in parts)
+        return PackedWeights(p0.format, p0.split, rows, p0.cols, rows, p0.orig_cols, streams,
+                             torch.cat([p.scales for p in parts]))
+
     def shard(self, tr0: int, tr1: int) -> "PackedWeights":
         """Tile-rows [tr0, tr1) as zero-copy views (tiles are stored in
         row-major tile order, prepack.cpp:190-191, so a tile-row range is one

@@ -897,3 +897,27 @@ def test_quantize_staged_and_two_pass_rows(cuda, oracle, dtype, e, m):
             with pytest.raises(fpx.FpxError) as ei:
                 fpx.quantize_matrix(t if dtype == "fp32" else t.half(), fpx.FpxFormat(e, m))
             assert ei.value.code == fpx.ErrorCode.InvalidValue and f"row {rows - 1}" in str(ei.value)
+
+
+def test_concat_rows_equals_separate_linears(cuda):
+    """PackedWeights.concat_rows (gate + up as one launch): every part's rows of
+    the merged linear are bit-identical to that part's own linear at the same
+    split_k (tiles and their K chunks do not interact)."""
+    fpx = _fpx()
+    g = torch.Generator(device=cuda)
+    g.manual_seed(3)
+    parts = [fpx.quantize_pack((torch.randn(r, 640, device=cuda, generator=g) * 0.02), fpx.FpxFormat.e3m2())
+             for r in (192, 64, 320)]
+    merged = fpx.PackedWeights.concat_rows(parts)
+    assert merged.rows == 576 and merged.cols == parts[0].cols
+    for n in (1, 16, 40):
+        b = torch.randn(n, 640, device=cuda, generator=g).half()
+        c = fpx.gemm_packed(merged, b, split_k=3)
+        r0 = 0
+        for p in parts:
+            ci = fpx.gemm_packed(p, b, split_k=3)
+            assert torch.equal(c[:, r0:r0 + p.rows], ci), (n, r0)
+            r0 += p.rows
+    with pytest.raises(fpx.FpxError):
+        fpx.PackedWeights.concat_rows([parts[0], fpx.quantize_pack(torch.randn(64, 128, device=cuda),
+                                                                   fpx.FpxFormat.e3m2())])
