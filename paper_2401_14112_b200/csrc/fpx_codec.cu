@@ -99,19 +99,20 @@ __device__ __forceinline__ uint32_t encode4(float4 v, float sv, float inv, int e
         return encode_exact(v.x, sv, inv, e, m, bias, cmax) | encode_exact(v.y, sv, inv, e, m, bias, cmax) << 8 |
                encode_exact(v.z, sv, inv, e, m, bias, cmax) << 16 | encode_exact(v.w, sv, inv, e, m, bias, cmax) << 24;
     } else {
+        // Signed quotients: the conversion rounds magnitudes and carries the
+        // sign (also of zero and of underflow to zero), exactly the
+        // reference's sign | magnitude code, so no sign bits are assembled.
         constexpr bool k5 = MODE == kEncHwE2M2;
         const float iv = k5 ? inv * 0.25f : inv;  // exact: a power-of-two factor
-        const float qa = fabsf(v.x) * iv, qb = fabsf(v.y) * iv, qc = fabsf(v.z) * iv, qd = fabsf(v.w) * iv;
+        const float qa = v.x * iv, qb = v.y * iv, qc = v.z * iv, qd = v.w * iv;
         constexpr float kUp = 1.0f + 0x1p-20f, kDn = 1.0f - 0x1p-20f;
         const uint32_t up = cvt_fp6x2<MODE>(qa * kUp, qb * kUp) | cvt_fp6x2<MODE>(qc * kUp, qd * kUp) << 16;
         const uint32_t dn = cvt_fp6x2<MODE>(qa * kDn, qb * kDn) | cvt_fp6x2<MODE>(qc * kDn, qd * kDn) << 16;
         if (up != dn)  // a quotient near a rounding boundary (rare: kept out of line)
             return encode4_exact_slow(v, sv, inv, e, m, bias, cmax);
-        const uint32_t sgn = ((__float_as_uint(v.x) >> 31) | (__float_as_uint(v.y) >> 31) << 8 |
-                              (__float_as_uint(v.z) >> 31) << 16 | (__float_as_uint(v.w) >> 31) << 24)
-                             << (k5 ? 4 : 5);
-        if constexpr (k5) return __vminu4(up & 0x1f1f1f1fu, 0x0f0f0f0fu) | sgn;
-        return (up & 0x1f1f1f1fu) | sgn;
+        // e2m2: sign bit 5 -> 4, magnitude saturated at 15 (7.0)
+        if constexpr (k5) return __vminu4(up & 0x1f1f1f1fu, 0x0f0f0f0fu) | ((up >> 1) & 0x10101010u);
+        return up & 0x3f3f3f3fu;
     }
 }
 
