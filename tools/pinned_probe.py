@@ -1,7 +1,7 @@
 """Steady-state H2D / D2H bandwidth of the e2e step's copy sizes from pinned
-host memory allocated three ways (GPU box only): torch pin_memory
-(cudaHostAlloc), and mmap'd memory registered with cudaHostRegister with and
-without transparent huge pages (madvise MADV_HUGEPAGE)."""
+host memory allocated several ways (GPU box only): torch pin_memory, mmap'd
+memory registered with cudaHostRegister with and without transparent huge
+pages (madvise MADV_HUGEPAGE), and cudaHostAlloc with each flag."""
 import ctypes
 import mmap
 import sys
@@ -12,7 +12,6 @@ libc = ctypes.CDLL("libc.so.6", use_errno=True)
 libc.mmap.restype = ctypes.c_void_p
 libc.mmap.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long]
 libc.madvise.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
-cudart = ctypes.CDLL("libcudart.so.12") if False else None
 MADV_HUGEPAGE = 14
 
 
