@@ -998,6 +998,7 @@ __global__ void __launch_bounds__(GCfg<F, NPAD, KS_, G_>::kThreads, 1)
         if (lane == 0) trace_cta(p, 13);  // after TMEM dealloc
     }
     if (p.split > 1) final_split_reduce<NPAD>(p, red_tq, red_n, C::kThreads);
+    if (FPX_TRACE && threadIdx.x == 0) trace_cta(p, 8);  // kernel exit (after the deferred reductions)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -29,8 +29,8 @@ splits = {n: fpx.default_split(M, K, n) for n in batches}
 ws = torch.zeros(int(max(L.fpx_linear_workspace_size(M, K, K, n, splits[n]) for n in batches)), dtype=torch.uint8,
                  device=dev)
 tot_a, tot_c = sum(batches) * K, sum(batches) * M
-h_act = torch.randn(tot_a).half().pin_memory()
-h_out = torch.empty(tot_c, pin_memory=True)
+h_act = bench.page_locked(torch, torch.randn(tot_a).half())
+h_out = bench.page_locked(torch, torch.empty(tot_c))
 d_act = [torch.randn(tot_a, device=dev).half() for _ in range(2)]
 d_out = [torch.empty(tot_c, device=dev) for _ in range(2)]
 aoff, coff, a, c = {}, {}, 0, 0

@@ -61,6 +61,6 @@ slow = np.argsort(-rel[:, 7])[:5]
 for i in slow:
     print("  slowest CTA", i, " ".join(f"{x:7.2f}" for x in rel[i]))
 names = {15: "entry", 0: "prologue", 14: "1st wstage", 1: "unit1 epi", 9: "mma done", 11: "epi done", 7: "sync",
-         12: "teardown", 13: "dealloc"}
+         12: "teardown", 13: "dealloc", 8: "exit"}
 print("per-CTA event medians (us from the earliest prologue):",
       " ".join(f"{nm}={np.nanmedian(rel[:, k]):.2f}" for k, nm in names.items() if np.any(~np.isnan(rel[:, k]))))
