@@ -921,3 +921,42 @@ def test_concat_rows_equals_separate_linears(cuda):
     with pytest.raises(fpx.FpxError):
         fpx.PackedWeights.concat_rows([parts[0], fpx.quantize_pack(torch.randn(64, 128, device=cuda),
                                                                    fpx.FpxFormat.e3m2())])
+
+
+def test_concurrent_streams_bit_identical(cuda):
+    """Linears on three streams at once -- split-K, wide and narrow batches,
+    each stream with its own workspace (the contract of fpx_c.h) -- plus a
+    fused quantize+pack on a fourth stream: every result is bit-identical to
+    the same call run alone."""
+    fpx = _fpx()
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    fmt = fpx.FpxFormat.e3m2()
+    packs = [fpx.quantize_pack(torch.randn(r, c, device=cuda, generator=g) * 0.02, fmt)
+             for r, c in ((1024, 2048), (768, 1536), (2048, 1024))]
+    jobs = []  # (pack, activations, split_k)
+    for i, n in enumerate((1, 16, 40, 130, 7, 256)):
+        p = packs[i % 3]
+        jobs.append((p, torch.randn(n, p.cols, device=cuda, generator=g).half(), (0, 3, 5)[i % 3]))
+    w_q = torch.randn(640, 1152, device=cuda, generator=g)
+    alone = [fpx.gemm_packed(p, b, split_k=sk) for p, b, sk in jobs]
+    q_alone = fpx.quantize_pack(w_q, fmt)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(cuda) for _ in range(4)]
+    outs = [[None] * len(jobs) for _ in range(3)]
+    q_out = []
+    for rep in range(3):
+        for si in range(3):
+            with torch.cuda.stream(streams[si]):
+                for j in range(si, len(jobs) + si):  # each stream its own order
+                    p, b, sk = jobs[j % len(jobs)]
+                    outs[si][j % len(jobs)] = fpx.gemm_packed(p, b, split_k=sk)
+        with torch.cuda.stream(streams[3]):
+            q_out.append(fpx.quantize_pack(w_q, fmt))
+    torch.cuda.synchronize()
+    for si in range(3):
+        for j, ref in enumerate(alone):
+            assert torch.equal(outs[si][j], ref), (si, j)
+    for q in q_out:
+        assert all(torch.equal(a, b) for a, b in zip(q.streams, q_alone.streams))
+        assert torch.equal(q.scales, q_alone.scales)
