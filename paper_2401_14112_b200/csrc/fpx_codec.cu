@@ -711,6 +711,69 @@ __global__ void __launch_bounds__(32 * kPackWarps) unpack_kernel(uint8_t* __rest
     }
 }
 
+// The two-segment splits ([2,4] FP6, [4,1] FP5) with persistent warps that
+// keep the next tile's packed words in flight (registers) while they unpack
+// the current one, as prepack_kernel does for the forward direction.
+template <int W>
+__device__ __forceinline__ void unpack_words(const uint32_t (&wd)[4 * W], uint32_t (&x)[32], int low) {
+    constexpr uint32_t kPer = 8u / W;
+    constexpr uint32_t kMask = ((1u << W) - 1u) * 0x01010101u;
+#pragma unroll
+    for (uint32_t j = 0; j < 4u * W; ++j)
+#pragma unroll
+        for (uint32_t g = 0; g < kPer; ++g) x[j * kPer + g] |= ((wd[j] >> (8u - W * (g + 1u))) & kMask) << low;
+}
+
+template <int W0, int W1>
+__global__ void __launch_bounds__(32 * kPackWarps) unpack2_kernel(uint8_t* __restrict__ codes, uint32_t cols_p,
+                                                                  uint32_t ntiles, const uint8_t* __restrict__ s0,
+                                                                  const uint8_t* __restrict__ s1) {
+    __shared__ __align__(16) uint8_t tile_s[kPackWarps][64 * kTileStride];
+    const uint32_t warp = threadIdx.x >> 5, t = threadIdx.x & 31u;
+    const uint32_t nw = gridDim.x * kPackWarps;
+    const uint32_t gc = cols_p / 64u;
+    uint8_t* ts = tile_s[warp];
+    auto load = [&](uint32_t tile, uint32_t (&a)[4 * W0], uint32_t (&b)[4 * W1]) {
+        const uint32_t* pa = reinterpret_cast<const uint32_t*>(s0 + static_cast<size_t>(tile) * 512u * W0);
+        const uint32_t* pb = reinterpret_cast<const uint32_t*>(s1 + static_cast<size_t>(tile) * 512u * W1);
+#pragma unroll
+        for (uint32_t j = 0; j < 4u * W0; ++j) a[j] = __ldcs(pa + j * 32u + t);
+#pragma unroll
+        for (uint32_t j = 0; j < 4u * W1; ++j) b[j] = __ldcs(pb + j * 32u + t);
+    };
+    uint32_t tile = blockIdx.x * kPackWarps + warp;
+    uint32_t ca[4 * W0], cb[4 * W1];
+    if (tile < ntiles) load(tile, ca, cb);
+    for (; tile < ntiles; tile += nw) {
+        uint32_t x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = 0u;
+        unpack_words<W0>(ca, x, W1);  // segment 0 holds the high bits
+        unpack_words<W1>(cb, x, 0);
+        if (tile + nw < ntiles) load(tile + nw, ca, cb);  // next tile in flight
+        const uint32_t r0 = (tile / gc) * 64u, c0 = (tile % gc) * 64u;
+#pragma unroll
+        for (uint32_t it = 0; it < 32u; ++it) {
+            const uint32_t sl = it >> 3, ch = (it >> 1) & 3u, ph = it & 1u;
+            const uint32_t rr = 16u * ch + t / 4u, cc = 16u * sl + 8u * ph + 2u * (t % 4u);
+            uint32_t a, b;
+            asm("prmt.b32 %0, %1, 0, 0x4431;" : "=r"(a) : "r"(x[it]));  // lanes 1, 3 -> row rr
+            asm("prmt.b32 %0, %1, 0, 0x4420;" : "=r"(b) : "r"(x[it]));  // lanes 0, 2 -> row rr + 8
+            *reinterpret_cast<uint16_t*>(ts + rr * kTileStride + cc) = static_cast<uint16_t>(a);
+            *reinterpret_cast<uint16_t*>(ts + (rr + 8u) * kTileStride + cc) = static_cast<uint16_t>(b);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t chunk = i * 32u + t;
+            const uint32_t rr = chunk >> 2, cc = (chunk & 3u) * 16u;
+            *reinterpret_cast<uint4*>(codes + static_cast<size_t>(r0 + rr) * cols_p + c0 + cc) =
+                *reinterpret_cast<const uint4*>(ts + rr * kTileStride + cc);
+        }
+        __syncwarp();  // ts is rewritten next iteration
+    }
+}
+
 // ------------------------------------------------------------------ K3
 // Verification de-quantiser.  Block = 2 warps = one 64x64 tile; warp h runs
 // exactly a register path of the fused kernel (dequant_slice_half<F, P>:
@@ -1070,8 +1133,15 @@ cudaError_t launch_unpack(const uint8_t* const* streams, uint32_t rows_p, uint32
                           const int* widths, uint8_t* codes, cudaStream_t st) {
     const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
     if (ntiles == 0) return cudaSuccess;
-    unpack_kernel<<<(ntiles + kPackWarps - 1) / kPackWarps, 32 * kPackWarps, 0, st>>>(
-        codes, cols_p, ntiles, bits, make_sdc(nseg, widths, streams));
+    const uint32_t blocks = std::min<uint32_t>((ntiles + kPackWarps - 1) / kPackWarps, 148u * 8u);
+    if (nseg == 2 && widths[0] == 2 && widths[1] == 4) {
+        unpack2_kernel<2, 4><<<blocks, 32 * kPackWarps, 0, st>>>(codes, cols_p, ntiles, streams[0], streams[1]);
+    } else if (nseg == 2 && widths[0] == 4 && widths[1] == 1) {
+        unpack2_kernel<4, 1><<<blocks, 32 * kPackWarps, 0, st>>>(codes, cols_p, ntiles, streams[0], streams[1]);
+    } else {
+        unpack_kernel<<<(ntiles + kPackWarps - 1) / kPackWarps, 32 * kPackWarps, 0, st>>>(
+            codes, cols_p, ntiles, bits, make_sdc(nseg, widths, streams));
+    }
     return cudaGetLastError();
 }
 
