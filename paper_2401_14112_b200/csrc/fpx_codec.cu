@@ -599,7 +599,9 @@ __global__ void __launch_bounds__(32 * kPackWarps) quantize_pack_kernel(const T*
     // only at the encode), so both dtypes keep 128 bytes per lane in flight;
     // row scales and skip flags load alongside and apply after.
     constexpr uint32_t kG = 16u / (4u * sizeof(T)), kLpr = 16u / kG, kRpp = 32u / kLpr;
-    constexpr uint32_t kChunk = 8u;
+    // 16-byte words in flight per lane: 8 for fp32 input, 4 for fp16 (its
+    // encode of 8 weights per word needs the registers; 87 -> 64 per thread)
+    constexpr uint32_t kChunk = sizeof(T) == 2 ? 4u : 8u;
     static_assert((64u / kRpp) % kChunk == 0, "passes per chunk");
     const uint32_t cc = (t % kLpr) * 4u * kG, c = c0 + cc;
     const bool full = c + 4u * kG <= cols;
