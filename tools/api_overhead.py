@@ -1,3 +1,7 @@
+"""Wall time of the Python API calls (quantize_matrix, pack, dequantize, unpack,
+quantize_pack) and of the raw C-ABI prepack with / without the scale check,
+plus a torch.profiler table (GPU box only).  Found the ~0.4 ms per-call
+cudaMallocAsync remap fixed by the library-owned scratch pool."""
 import time, torch, ctypes as C, sys
 sys.path.insert(0, '.')
 import paper_2401_14112_b200 as fpx
