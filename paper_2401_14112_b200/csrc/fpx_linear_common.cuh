@@ -165,47 +165,110 @@ __device__ __forceinline__ void final_split_reduce(const KParams& p, const uint3
                                                    uint32_t nthreads) {
     const uint32_t n0 = red_n[0], n1 = red_n[1], n2 = red_n[2], n3 = red_n[3];
     const uint32_t npend = n0 + n1 + n2 + n3;
-    const uint32_t nsl = (p.n + 3) / 4;
-    const uint32_t items = npend * 32 * nsl;
-    const size_t cstride = static_cast<size_t>(kTileM) * NPAD;
-    const uint64_t pol_drop = policy_evict_first();
-    for (uint32_t it = threadIdx.x; it < items; it += nthreads) {
-        const uint32_t rl = it & 31u, rest = it >> 5;
-        const uint32_t sl = rest % nsl, pi = rest / nsl;
-        // pi-th pending pair: quarter lists are concatenated in quarter order
-        uint32_t q = 0, idx = pi;
-        if (idx >= n0) {
-            idx -= n0, q = 1;
-            if (idx >= n1) {
-                idx -= n1, q = 2;
-                if (idx >= n2) idx -= n2, q = 3;
+    // NPAD 16 keeps 4-column items (its kernel is left byte-identical: the
+    // decode kernel is sensitive to code layout); wider batches use
+    // 8-column items so that N = 32 fits one round of the CTA's threads.
+    if constexpr (NPAD <= 16) {
+        const uint32_t nsl = (p.n + 3) / 4;
+        const uint32_t items = npend * 32 * nsl;
+        const size_t cstride = static_cast<size_t>(kTileM) * NPAD;
+        const uint64_t pol_drop = policy_evict_first();
+        for (uint32_t it = threadIdx.x; it < items; it += nthreads) {
+            const uint32_t rl = it & 31u, rest = it >> 5;
+            const uint32_t sl = rest % nsl, pi = rest / nsl;
+            // pi-th pending pair: quarter lists are concatenated in quarter order
+            uint32_t q = 0, idx = pi;
+            if (idx >= n0) {
+                idx -= n0, q = 1;
+                if (idx >= n1) {
+                    idx -= n1, q = 2;
+                    if (idx >= n2) idx -= n2, q = 3;
+                }
+            }
+            const uint32_t tq = red_tq[q * kMaxDefer + idx];
+            const uint32_t mt = tq >> 2, row_l = 32 * (tq & 3u) + rl;
+            const float* base = p.ws + static_cast<size_t>(mt) * p.split * cstride + sl * kTileM * 4 + row_l * 4;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            constexpr uint32_t kInFlight = 12;
+            for (uint32_t cb = 0; cb < p.split; cb += kInFlight) {
+                float4 t[kInFlight];
+    #pragma unroll
+                for (uint32_t u = 0; u < kInFlight; ++u)
+                    if (cb + u < p.split) t[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride, pol_drop);
+    #pragma unroll
+                for (uint32_t u = 0; u < kInFlight; ++u)
+                    if (cb + u < p.split) {
+                        acc.x += t[u].x;
+                        acc.y += t[u].y;
+                        acc.z += t[u].z;
+                        acc.w += t[u].w;
+                    }
+            }
+            const uint32_t m = mt * kTileM + row_l;
+            if (m < p.rows_p) {
+                const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+    #pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (4 * sl + j < p.n) c_store(p, m, 4 * sl + j, a4[j]);
             }
         }
-        const uint32_t tq = red_tq[q * kMaxDefer + idx];
-        const uint32_t mt = tq >> 2, row_l = 32 * (tq & 3u) + rl;
-        const float* base = p.ws + static_cast<size_t>(mt) * p.split * cstride + sl * kTileM * 4 + row_l * 4;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        constexpr uint32_t kInFlight = 12;
-        for (uint32_t cb = 0; cb < p.split; cb += kInFlight) {
-            float4 t[kInFlight];
-#pragma unroll
-            for (uint32_t u = 0; u < kInFlight; ++u)
-                if (cb + u < p.split) t[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride, pol_drop);
-#pragma unroll
-            for (uint32_t u = 0; u < kInFlight; ++u)
-                if (cb + u < p.split) {
-                    acc.x += t[u].x;
-                    acc.y += t[u].y;
-                    acc.z += t[u].z;
-                    acc.w += t[u].w;
+    } else {
+        // an item is 8 columns (two 4-column slices) of one row: N = 32 then
+        // needs 512 items per 4 pending pairs -- one round of the CTA's threads
+        // and one L2 round trip (4-column items took two)
+        const uint32_t nsl = (p.n + 7) / 8;
+        const uint32_t items = npend * 32 * nsl;
+        const size_t cstride = static_cast<size_t>(kTileM) * NPAD;
+        const uint64_t pol_drop = policy_evict_first();
+        for (uint32_t it = threadIdx.x; it < items; it += nthreads) {
+            const uint32_t rl = it & 31u, rest = it >> 5;
+            const uint32_t sl = rest % nsl, pi = rest / nsl;
+            // pi-th pending pair: quarter lists are concatenated in quarter order
+            uint32_t q = 0, idx = pi;
+            if (idx >= n0) {
+                idx -= n0, q = 1;
+                if (idx >= n1) {
+                    idx -= n1, q = 2;
+                    if (idx >= n2) idx -= n2, q = 3;
                 }
-        }
-        const uint32_t m = mt * kTileM + row_l;
-        if (m < p.rows_p) {
-            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (4 * sl + j < p.n) c_store(p, m, 4 * sl + j, a4[j]);
+            }
+            const uint32_t tq = red_tq[q * kMaxDefer + idx];
+            const uint32_t mt = tq >> 2, row_l = 32 * (tq & 3u) + rl;
+            const bool hi = 8 * sl + 4 < p.n;  // the second 4-column slice exists
+            const float* base = p.ws + static_cast<size_t>(mt) * p.split * cstride + 2 * sl * kTileM * 4 + row_l * 4;
+            float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+            constexpr uint32_t kInFlight = 4;
+            for (uint32_t cb = 0; cb < p.split; cb += kInFlight) {
+                float4 t0[kInFlight], t1[kInFlight];
+    #pragma unroll
+                for (uint32_t u = 0; u < kInFlight; ++u) {
+                    if (cb + u < p.split) t0[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride, pol_drop);
+                    if (hi && cb + u < p.split)
+                        t1[u] = ld_global_cg_v4_hint(base + (cb + u) * cstride + kTileM * 4, pol_drop);
+                }
+    #pragma unroll
+                for (uint32_t u = 0; u < kInFlight; ++u) {
+                    if (cb + u < p.split) {
+                        acc0.x += t0[u].x;
+                        acc0.y += t0[u].y;
+                        acc0.z += t0[u].z;
+                        acc0.w += t0[u].w;
+                    }
+                    if (hi && cb + u < p.split) {
+                        acc1.x += t1[u].x;
+                        acc1.y += t1[u].y;
+                        acc1.z += t1[u].z;
+                        acc1.w += t1[u].w;
+                    }
+                }
+            }
+            const uint32_t m = mt * kTileM + row_l;
+            if (m < p.rows_p) {
+                const float a8[8] = {acc0.x, acc0.y, acc0.z, acc0.w, acc1.x, acc1.y, acc1.z, acc1.w};
+    #pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (8 * sl + j < p.n) c_store(p, m, 8 * sl + j, a8[j]);
+            }
         }
     }
 }
