@@ -960,3 +960,18 @@ def test_concurrent_streams_bit_identical(cuda):
     for q in q_out:
         assert all(torch.equal(a, b) for a, b in zip(q.streams, q_alone.streams))
         assert torch.equal(q.scales, q_alone.scales)
+
+
+@pytest.mark.parametrize("e,m", [(3, 2), (2, 3), (2, 2)])
+def test_unpack_full_size_round_trip(cuda, e, m):
+    """unpack(pack(q)) == q at 8192 x 22016, where the persistent unpack
+    kernel's warps walk many tiles each (the small-case tests give every warp
+    at most one), and at a shape whose tile count is not a multiple of the
+    grid."""
+    fpx = _fpx()
+    g = torch.Generator(device=cuda)
+    g.manual_seed(17 + e)
+    for rows, cols in ((8192, 22016), (4160, 6016)):
+        q = fpx.quantize_matrix(torch.randn(rows, cols, device=cuda, generator=g), fpx.FpxFormat(e, m))
+        u = fpx.unpack(fpx.pack(q))
+        assert torch.equal(u.codes, q.codes), (rows, cols)
