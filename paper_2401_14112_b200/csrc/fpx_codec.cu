@@ -1122,14 +1122,15 @@ cudaError_t launch_quantize_pack(const void* w, int w_dtype, uint32_t rows, uint
     return cudaGetLastError();
 }
 
-cudaError_t launch_prepack(const uint8_t* codes, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,
-                           const int* widths, uint8_t* const* streams, cudaStream_t st) {
-    const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
-    if (ntiles == 0) return cudaSuccess;
 // persistent CTAs per SM for the pack / unpack kernels: 11 x 20 KB of
 // staging fills the SM's shared memory (measured 8 -> 11: prepack 59.8 ->
 // 57.1 us, unpack 56.7 -> 53.6 us at 8192 x 22016)
 constexpr uint32_t kPackCtasPerSm = 11;
+
+cudaError_t launch_prepack(const uint8_t* codes, uint32_t rows_p, uint32_t cols_p, int bits, int nseg,
+                           const int* widths, uint8_t* const* streams, cudaStream_t st) {
+    const uint32_t ntiles = (rows_p / 64u) * (cols_p / 64u);
+    if (ntiles == 0) return cudaSuccess;
     const uint32_t blocks = std::min<uint32_t>((ntiles + kPackWarps - 1) / kPackWarps, 148u * kPackCtasPerSm);
     prepack_kernel<<<blocks, 32 * kPackWarps, 0, st>>>(codes, cols_p, ntiles, bits, make_sd(nseg, widths, streams));
     return cudaGetLastError();
