@@ -101,3 +101,31 @@ def test_shard_layout_covers_all_rows():
             row0, nrows, m_slot = shard.shard_layout(rows_p, world)
             assert sum(nrows) == rows_p and m_slot == max(nrows)
             assert all(row0[i] + nrows[i] == row0[i + 1] for i in range(world - 1))
+
+
+def test_concat_rows_is_shard_inverse():
+    """PackedWeights.concat_rows (merged gate/up, Q/K/V) is the byte-level
+    inverse of shard(): concatenating the tile-row shards of a packed weight
+    gives back its streams and scales exactly, and mismatched parts are
+    rejected (host logic; the GPU bit-identity of the merged linear is
+    tests/test_gpu_parity.py::test_concat_rows_equals_separate_linears)."""
+    from oracle.oracle import Oracle
+    from paper_2401_14112_b200.fpx import FpxError
+    O = Oracle()
+    rng = np.random.default_rng(5)
+    rows, cols = 320, 256
+    w = (rng.standard_normal((rows, cols)) * 0.02).astype(np.float32)
+    st, codes, scales, _ = O.quantize(w, 3, 2)
+    st, streams = O.pack(codes, scales, 3, 2)
+    p = PackedWeights(FpxFormat(3, 2), SplitScheme((2, 4)), rows, cols, rows, cols,
+                      [torch.from_numpy(s) for s in streams], torch.from_numpy(scales.view(np.int16)))
+    parts = [p.shard(0, 1), p.shard(1, 3), p.shard(3, 5)]
+    q = PackedWeights.concat_rows(parts)
+    assert q.rows == rows and q.cols == cols
+    assert all(torch.equal(a, b) for a, b in zip(q.streams, p.streams))
+    assert torch.equal(q.scales, p.scales)
+    other = PackedWeights(FpxFormat(3, 2), SplitScheme((2, 4)), 64, 128, 64, 128,
+                          [torch.zeros(64 * 128 * 2 // 8, dtype=torch.uint8),
+                           torch.zeros(64 * 128 * 4 // 8, dtype=torch.uint8)], torch.zeros(64, dtype=torch.int16))
+    with pytest.raises(FpxError):
+        PackedWeights.concat_rows([parts[0], other])
