@@ -610,12 +610,15 @@ def run_ours(args, rank, world, local):
         g_e2e = ctx.capture(e2e_steps)
         e2e_ms = ctx.max_over_ranks(ctx.timed(g_e2e))
         del g_e2e
+        torch.cuda.synchronize(dev)
+        for h in (h_act_all, h_out_all):
+            torch.cuda.cudart().cudaHostUnregister(h.data_ptr())  # no-op error if pin_memory() was the fallback
         h2d = tot_a * 2
         d2h = tot_c * 4
         e2e = {"value": round(world * nl * WEIGHT_BYTES / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(e2e_ms / args.steps, 4),
-               "note": "per step: one H2D of the six batches' pinned host activations (copy stream) + the six "
+               "note": "per step: one H2D of the six batches' page-locked (cudaHostRegister) host activations (copy stream) + the six "
                        + ("fpx_linear_sharded calls (C-ABI: shard kernel + NCCL all-gather + scatter, compute stream)"
                           if world > 1 else "fpx_linear calls (C-ABI, compute stream)")
                        + " + one D2H of their fp32 outputs (second copy stream), double-buffered so copies overlap "
