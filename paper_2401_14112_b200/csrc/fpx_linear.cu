@@ -1243,10 +1243,11 @@ int linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n, int num_s
     best_s = pick(10.0);
     // Where even that split gives CTAs several units, their boundaries cost
     // less than the fit above assumes (the round-2 unit table and deferred
-    // reductions): re-pick with a 4-k-tile penalty (70B QKV 10240x8192 at
-    // N=16: split 3 -> 5, 16.4 -> 15.5 us).  One-unit-per-CTA shapes, the
-    // headline among them, keep the first pick.
-    if (std::ceil(double(tiles_m) * best_s / num_sms) > 1.0) best_s = pick(4.0);
+    // reductions): re-pick with a 2-k-tile penalty (70B QKV 10240x8192 at
+    // N=16: split 3 -> 5, 16.4 -> 15.9 us; gate/up 28672x8192 at N=1:
+    // 3 -> 5, 31.9 -> 30.9 us).  One-unit-per-CTA shapes, the headline among
+    // them, keep the first pick.
+    if (std::ceil(double(tiles_m) * best_s / num_sms) > 1.0) best_s = pick(2.0);
     (void)best;
     return best_s;
 }
