@@ -1229,25 +1229,26 @@ int linear_default_split(uint32_t rows_p, uint32_t cols_p, uint32_t n, int num_s
     // §8d's shapes (bench_configs.py --sweep-splits: 8192x22016, 22016x8192,
     // the five 70B linears, 4096^2); it makes fewer, longer units win over
     // finer load balance.  Split-K partial traffic adds a little per unit.
-    auto pick = [&](double unit_pen) {
+    auto pick = [&](double unit_pen, double part_w, bool finer_on_tie) {
         double b = 1e30;
         int bs = 1;
         for (int s = 1; s <= smax; ++s) {
             const double per_cta = std::ceil(double(tiles_m) * s / num_sms);
-            const double pen = unit_pen + (s > 1 ? 0.25 * (2.0 * kTileM * n * 4.0) / 6144.0 : 0.0);
+            const double pen = unit_pen + (s > 1 ? part_w * (2.0 * kTileM * n * 4.0) / 6144.0 : 0.0);
             const double est = per_cta * (std::ceil(double(kt) / s) + pen);
-            if (est < b - 1e-9) b = est, bs = s;
+            if (est < b - 1e-9 || (finer_on_tie && est <= b + 1e-9)) b = est, bs = s;
         }
         return bs;
     };
-    best_s = pick(10.0);
+    best_s = pick(10.0, 0.25, false);
     // Where even that split gives CTAs several units, their boundaries cost
     // less than the fit above assumes (the round-2 unit table and deferred
-    // reductions): re-pick with a 2-k-tile penalty (70B QKV 10240x8192 at
-    // N=16: split 3 -> 5, 16.4 -> 15.9 us; gate/up 28672x8192 at N=1:
-    // 3 -> 5, 31.9 -> 30.9 us).  One-unit-per-CTA shapes, the headline among
-    // them, keep the first pick.
-    if (std::ceil(double(tiles_m) * best_s / num_sms) > 1.0) best_s = pick(2.0);
+    // reductions): re-pick with a 2-k-tile penalty, half the partial-traffic
+    // weight and ties to the finer split (N=16: 70B QKV 10240x8192 split 3 -> 5, 16.4 -> 15.9
+    // us; gate/up 28672x8192 3 -> 5, 33.1 -> 32.5 us; 22016x8192 4 -> 5,
+    // 26.8 -> 26.0 us).  One-unit-per-CTA shapes, the headline among them,
+    // keep the first pick.
+    if (std::ceil(double(tiles_m) * best_s / num_sms) > 1.0) best_s = pick(2.0, 0.125, true);
     (void)best;
     return best_s;
 }
