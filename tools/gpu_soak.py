@@ -3,7 +3,7 @@ rotated weight copies, replayed REPS times, for every routed batch width and
 the three fused formats at default and forced splits; every output compared
 bit for bit with a single reference launch.  Prints one line per case and
 `soak ok` at the end; run it under `timeout` (a hang is the failure mode it
-hunts).  env: REPS (50)."""
+hunts).  env: REPS (50), KM / KK (weight shape, 4096 x 6144), NS (batch widths)."""
 import os
 import sys
 import time
@@ -16,14 +16,16 @@ import paper_2401_14112_b200 as fpx  # noqa: E402
 
 dev = torch.device("cuda:0")
 reps = int(os.environ.get("REPS", 50))
+KM, KK = int(os.environ.get("KM", 4096)), int(os.environ.get("KK", 6144))
+NS = [int(x) for x in os.environ.get("NS", "1,7,16,17,32,48,64,100,128,200").split(",")]
 total = 0
 t0 = time.time()
 for (e, m) in ((3, 2), (2, 3), (2, 2)):
     torch.manual_seed(e * 10 + m)
-    p0 = fpx.quantize_pack(torch.randn(4096, 6144, device=dev) * 0.02, fpx.FpxFormat(e, m))
+    p0 = fpx.quantize_pack(torch.randn(KM, KK, device=dev) * 0.02, fpx.FpxFormat(e, m))
     copies = [p0] + [fpx.PackedWeights(p0.format, p0.split, p0.rows, p0.cols, p0.orig_rows, p0.orig_cols,
                                        [s.clone() for s in p0.streams], p0.scales.clone()) for _ in range(2)]
-    for n in (1, 7, 16, 17, 32, 48, 64, 100, 128, 200):
+    for n in NS:
         for sk in (0, 3, 7):
             x = torch.randn(n, p0.cols, device=dev).half()
             ref = fpx.gemm_packed(p0, x, split_k=sk)
